@@ -1,0 +1,206 @@
+/* ppx.h — C ABI of libppx.so, the B200 (sm_100a) phantom-parallel FFN engine.
+ *
+ * Drop-in boundary for the hot path of arXiv 2508.00960's reference simulator `phantomsim`
+ * (/root/reference/pkg/src/phantomsim).  The reference is pure Python/numpy; its "FFI" for this
+ * path is the Python function surface exported by phantomsim/__init__.py:5-33.  Every entry point
+ * below replaces one of those functions (or the device half of one), cited per declaration; the
+ * Python package paper_2508_00960_b200 binds them with ctypes (INTEGRATION.md shows the stub a
+ * phantomsim maintainer would add).
+ *
+ * Conventions
+ *  - All matrices are row-major on the device with an explicit leading dimension in elements
+ *    (a multiple of 8).  The reference stores (features x batch) with batch as columns
+ *    (core.py:3-4); this ABI stores (batch x features), i.e. the transpose, so activations are
+ *    [B, s] and weights keep the reference's (out x in) orientation.
+ *  - dtype PPX_BF16: bf16 operands, fp32 accumulation (tcgen05 kind::f16).
+ *    dtype PPX_FP32: fp32 operands through 3xTF32 on tcgen05 kind::tf32 (hi*hi + hi*lo + lo*hi).
+ *  - Calls are asynchronous on `stream` (a cudaStream_t); the caller owns every buffer.
+ *    A ctx is not re-entrant; collectives must be issued in the same order on every GPU
+ *    (the Communicator contract, collectives.py:88-94).
+ *  - Status codes map onto phantomsim.errors (errors.py:4-29):
+ *    PPX_E_CONFIG -> ConfigurationError, PPX_E_PROTOCOL -> ProtocolError,
+ *    PPX_E_SEQUENCING -> SequencingError, PPX_E_NONFINITE -> TrainingError.
+ *
+ * Per-(rank, layer) parameter block ("flat layout").  One contiguous buffer in the PSHARD01
+ * record order of checkpoint.py:57-64 (local, compressor, decompressors ascending source rank
+ * with self skipped, bias), with lds = round8(s), ldk = round8(k):
+ *    local        [s, lds]            at 0
+ *    compressor   [k, lds]            at s*lds
+ *    decompressor [p-1][s, ldk]       at (s+k)*lds          (block q <-> source rank q + (q >= rank))
+ *    bias         [s]                 at (s+k)*lds + (p-1)*s*ldk
+ *    total        ppx_layer_elems(s, k, p)
+ * When s and k are multiples of 8 this is byte-for-byte the PSHARD01 record (in the element
+ * type of the buffer).  Gradients, fp32 master weights and Adam moments use the same layout.
+ *
+ * Phantom buffers ("slots"): [p][B, ldk] with slot stride B*ldk; slot i holds rank i's k-wide
+ * block (collectives.py:337-339 all-gather order; phantom.py:155 dict view).
+ */
+#ifndef PPX_H_
+#define PPX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PPX_ABI_VERSION 1
+
+typedef struct ppx_ctx ppx_ctx;
+
+typedef enum {
+  PPX_OK = 0,
+  PPX_E_CONFIG = 1,
+  PPX_E_PROTOCOL = 2,
+  PPX_E_SEQUENCING = 3,
+  PPX_E_NONFINITE = 4,
+  PPX_E_CUDA = 5
+} ppx_status;
+
+typedef enum { PPX_BF16 = 0, PPX_FP32 = 1 } ppx_dtype;
+typedef enum { PPX_RELU = 0, PPX_IDENTITY = 1 } ppx_act; /* core.py:64-82 Activation */
+
+typedef enum { PPX_UPDATE_NONE = 0, PPX_UPDATE_SGD = 1, PPX_UPDATE_ADAM = 2 } ppx_update_kind;
+
+/* One logical rank's shard of one layer (phantom.py:23-54 PhantomLayer). */
+typedef struct {
+  int32_t s, k, p, rank;
+  const void* w;        /* flat parameter block in the call's dtype (what the GEMMs read) */
+  const float* master;  /* flat fp32 block; the bias is read from here (may equal w for FP32) */
+} ppx_layer;
+
+/* Optimizer fused into the weight-gradient epilogue (training.py:74-105). */
+typedef struct {
+  int32_t kind;          /* ppx_update_kind */
+  const float* hyper;    /* device: [lr, beta1, beta2, eps, 1-beta1^t, 1-beta2^t] */
+  float* master;         /* flat fp32 master, updated in place */
+  void* w_next;          /* flat copy in the compute dtype written from the new master (NULL: none) */
+  float* adam_m;         /* flat fp32 first moment (Adam) */
+  float* adam_v;         /* flat fp32 second moment (Adam) */
+  float* grad;           /* optional flat fp32 raw-gradient output (NULL: not stored) */
+  int* bad;              /* device flag set to 1 on a non-finite gradient (NULL: unchecked) */
+} ppx_update;
+
+/* Generic epilogue for ppx_gemm (the Megatron TP comparison pipeline reuses it). */
+typedef struct {
+  int32_t act;           /* ppx_act applied after bias */
+  const float* bias;     /* [N] or NULL */
+  int32_t accumulate;    /* C += result */
+  const void* mask;      /* multiply by (mask[m, n] > 0), same dtype as C, or NULL */
+  int64_t ld_mask;
+  float* colsum;         /* += column sums of the stored result, or NULL */
+} ppx_epilogue;
+
+/* ---- context / communicator (collectives.py:87-194 Communicator -> NCCL over NVLink) ---- */
+int ppx_abi_version(void);
+int64_t ppx_layer_elems(int32_t s, int32_t k, int32_t p);
+ppx_status ppx_get_unique_id(uint8_t uid[128]);
+/* world GPUs, this process drives GPU `rank` on CUDA device `device`; uid from rank 0
+   (ignored when world == 1). */
+ppx_status ppx_create(int32_t world, int32_t rank, int32_t device, const uint8_t* uid, ppx_ctx** out);
+ppx_status ppx_destroy(ppx_ctx* ctx);
+const char* ppx_last_error(const ppx_ctx* ctx);
+int32_t ppx_num_sms(const ppx_ctx* ctx);
+
+/* ---- phantom-parallel layer ops -------------------------------------------------------- */
+
+/* phantom.py:153 — own phantom block g = C . y_prev, written to phantoms slot `rank`. */
+ppx_status ppx_compress(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B,
+                        const void* y_prev, int64_t ld_y, void* phantoms, void* stream);
+
+/* collectives.py:115-120 / 337-339 — in-place all-gather of the phantom slots.  This GPU owns
+   `local_ranks` consecutive logical ranks starting at rank*local_ranks; slot_elems = B*ldk. */
+ppx_status ppx_all_gather(ppx_ctx* ctx, ppx_dtype dt, void* phantoms, int64_t slot_elems,
+                          int32_t local_ranks, void* stream);
+
+/* phantom.py:152-163 — y = act(L.y_prev + sum_{i != rank asc} D_i.g_i + b), ONE K-concatenated
+   tcgen05 contraction over [y_prev | g_peers]; optional pre-activation output. */
+ppx_status ppx_forward_update(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, ppx_act act,
+                              const void* y_prev, int64_t ld_y, const void* phantoms,
+                              void* y_out, int64_t ld_out, void* preact, int64_t ld_pre, void* stream);
+
+/* phantom.py:152-182 + training.py:59-71,195-199 — the output layer's update fused with the
+   output delta, the half-squared loss partial and the output bias gradient:
+     y = act(pre); delta = (y - t) * act'(pre) * delta_scale; *loss += loss_scale * sum (y-t)^2;
+     bias_grad += sum_batch delta (if non-NULL). */
+ppx_status ppx_forward_output(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, ppx_act act,
+                              const void* y_prev, int64_t ld_y, const void* phantoms,
+                              void* y_out, int64_t ld_out, const void* target, int64_t ld_t,
+                              void* delta, int64_t ld_d, float delta_scale, float loss_scale,
+                              float* loss, float* bias_grad, void* stream);
+
+/* phantom.py:169-182 (+ training.py:66-69 scaling) — standalone output delta and loss partial.
+   `pre` is the pre-activation (or the layer output: ReLU'(pre) == (y > 0)). */
+ppx_status ppx_output_delta(ppx_ctx* ctx, ppx_dtype dt, int32_t B, int32_t s, ppx_act act,
+                            const void* y_out, int64_t ld_y, const void* target, int64_t ld_t,
+                            const void* pre, int64_t ld_p, void* delta, int64_t ld_d,
+                            float delta_scale, float loss_scale, float* loss, void* stream);
+
+/* phantom.py:199-205 — slot i (i != rank) of contrib = D_i^T . delta, i.e. [B, k] = delta . D_i.
+   accumulate != 0 adds into contrib (several logical ranks on one GPU sum their slots in
+   ascending rank order before the cross-GPU reduce-scatter). The own slot is not written. */
+ppx_status ppx_error_phantoms(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B,
+                              const void* delta, int64_t ld_d, void* contrib, int32_t accumulate,
+                              void* stream);
+
+/* collectives.py:122-127 / 345-357 — in-place reduce-scatter of the contribution slots: after
+   it, slot j of `contrib` (for this GPU's local ranks) is the sum over all GPUs. */
+ppx_status ppx_reduce_scatter(ppx_ctx* ctx, ppx_dtype dt, void* contrib, int64_t slot_elems,
+                              int32_t local_ranks, void* stream);
+
+/* collectives.py:138-142 — elementwise fp32 sum over GPUs, in place (the scalar loss,
+   training.py:70). */
+ppx_status ppx_all_reduce_f32(ppx_ctx* ctx, float* buf, int64_t count, void* stream);
+/* same, in the compute dtype (Megatron TP all-reduce of activations / input gradients) */
+ppx_status ppx_all_reduce(ppx_ctx* ctx, ppx_dtype dt, void* buf, int64_t count, void* stream);
+
+/* phantom.py:239-267 — parameter gradients of one layer (fp32, flat layout `grad`):
+     local = delta^T y_prev, compressor = r^T y_prev, decompressor_i = delta^T g_i,
+     bias = sum_batch delta.   received r is [B, ldk] (slot `rank` of the reduced buffer).
+   With upd != NULL and upd->kind != NONE the optimizer is applied in the same epilogue
+   (bias excluded: see ppx_bias_update); grad may then be NULL. */
+ppx_status ppx_param_grads(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B,
+                           const void* delta, int64_t ld_d, const void* y_prev, int64_t ld_y,
+                           const void* phantoms, const void* received, float* grad,
+                           const ppx_update* upd, int32_t with_bias, void* stream);
+
+/* phantom.py:210-236 — delta_prev = (local^T delta + compressor^T r) * act'(pre_prev): ONE
+   K-concatenated contraction [delta | r] . [L ; C]; `mask_src` is pre_prev or y_prev (only its
+   sign is read; NULL for IDENTITY).  bias_grad_prev += sum_batch delta_prev if non-NULL. */
+ppx_status ppx_backward_delta(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, ppx_act act_prev,
+                              const void* delta, int64_t ld_d, const void* received,
+                              const void* mask_src, int64_t ld_m, void* delta_prev, int64_t ld_dp,
+                              float* bias_grad_prev, void* stream);
+
+/* phantom.py:253 — bias gradient alone: out[j] (+)= sum_b x[b, j]. */
+ppx_status ppx_colsum(ppx_ctx* ctx, ppx_dtype dt, int32_t rows, int32_t cols, const void* x, int64_t ld,
+                      float* out, int32_t accumulate, void* stream);
+
+/* training.py:74-82 / 92-105 — elementwise SGD / Adam over one fp32 array (params -= ...),
+   non-finite gradients flag *bad.  w_copy (optional) receives the new params in `dt`. */
+ppx_status ppx_optimizer_step(ppx_ctx* ctx, int32_t kind, const float* hyper, float* params,
+                              const float* grad, float* adam_m, float* adam_v, int64_t n,
+                              ppx_dtype dt, void* w_copy, int* bad, void* stream);
+
+/* core.py:39-61 gemm: C[M,N] = op(a) . op(b), op(a) = a [M,K] or a^T (a stored [K,M]),
+   op(b) = b [K,N] or b^T (b stored [N,K]).  out_dt selects C's element type. */
+ppx_status ppx_gemm(ppx_ctx* ctx, ppx_dtype dt, int32_t M, int32_t N, int32_t K,
+                    const void* a, int64_t lda, int32_t trans_a, const void* b, int64_t ldb,
+                    int32_t trans_b, void* c, int64_t ldc, ppx_dtype out_dt,
+                    const ppx_epilogue* epi, void* stream);
+
+/* elementwise helpers used by the host engine */
+ppx_status ppx_cast(ppx_ctx* ctx, ppx_dtype src_dt, const void* src, ppx_dtype dst_dt, void* dst,
+                    int64_t n, void* stream);
+/* y = act(x + bias) over [rows, cols] (TP row-parallel epilogue after the all-reduce);
+   y may alias x */
+ppx_status ppx_bias_act(ppx_ctx* ctx, ppx_dtype dt, int32_t rows, int32_t cols, const void* x,
+                        int64_t ldx, const float* bias, ppx_act act, void* y, int64_t ldy, void* stream);
+/* out[i] = mask ? (x[i] if mask_src[i] > 0 else 0) : x  — ReLU' applied in place */
+ppx_status ppx_relu_mask(ppx_ctx* ctx, ppx_dtype dt, int32_t rows, int32_t cols, void* x, int64_t ldx,
+                         const void* mask_src, int64_t ldm, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PPX_H_ */

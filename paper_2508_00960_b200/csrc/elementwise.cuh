@@ -1,0 +1,206 @@
+// Bandwidth-bound helper kernels of the phantom-parallel engine (everything that is not a
+// tensor-core contraction).  All are grid-stride / 2D-tiled, vector-friendly and launched on the
+// caller's stream.  References: phantom.py:169-182 (output delta), phantom.py:253 (bias grad),
+// training.py:74-105 (SGD / Adam), core.py:64-98 (activations).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ppx {
+
+struct GemmParams;
+template <bool kTF32>
+cudaError_t launch_gemm(const GemmParams& P, int grid, cudaStream_t st);
+
+__device__ __forceinline__ float ld_elem(const void* p, int64_t i, bool f32) {
+  return f32 ? reinterpret_cast<const float*>(p)[i] : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);
+}
+__device__ __forceinline__ void st_elem(void* p, int64_t i, bool f32, float v) {
+  if (f32) reinterpret_cast<float*>(p)[i] = v;
+  else reinterpret_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(v);
+}
+
+inline int ew_grid(int64_t n, int threads = 256) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > 148 * 16) g = 148 * 16;
+  return (int)(g < 1 ? 1 : g);
+}
+
+// ---- 3xTF32 operand split: hi = x with the low 13 mantissa bits cleared, lo = x - hi ----------
+__global__ void split_tf32_kernel(const float* __restrict__ x, float* __restrict__ hi, float* __restrict__ lo,
+                                  int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float v = x[i];
+    float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    hi[i] = h;
+    lo[i] = v - h;
+  }
+}
+inline void launch_split_tf32(const float* x, float* hi, float* lo, int64_t n, cudaStream_t st) {
+  split_tf32_kernel<<<ew_grid(n), 256, 0, st>>>(x, hi, lo, n);
+}
+
+// ---- transposing split: x [slots][rows][cols] (ld, ss) -> hi/lo [slots][cols][rows] (ldo, sso) ----
+// The FP32 tier feeds kind::tf32 only K-major operands (MN-major tf32 operands read as zeros on
+// sm_100a in our measurements), so MN-major fp32 operands are transposed while being split.
+__global__ void split_tf32_t_kernel(const float* __restrict__ x, int rows, int cols, int64_t ld, int64_t ss,
+                                    float* __restrict__ hi, float* __restrict__ lo, int64_t ldo, int64_t sso) {
+  __shared__ float tile[32][33];
+  const int slot = blockIdx.z;
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const float* xs = x + slot * ss;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int r = r0 + i, c = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = (r < rows && c < cols) ? xs[(int64_t)r * ld + c] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int c = c0 + i, r = r0 + threadIdx.x;  // output row = c, output col = r
+    if (c < cols && r < rows) {
+      float v = tile[threadIdx.x][i];
+      float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+      hi[slot * sso + (int64_t)c * ldo + r] = h;
+      lo[slot * sso + (int64_t)c * ldo + r] = v - h;
+    }
+  }
+}
+inline void launch_split_tf32_t(const float* x, int slots, int rows, int cols, int64_t ld, int64_t ss, float* hi,
+                                float* lo, int64_t ldo, int64_t sso, cudaStream_t st) {
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32, slots);
+  split_tf32_t_kernel<<<grid, dim3(32, 8), 0, st>>>(x, rows, cols, ld, ss, hi, lo, ldo, sso);
+}
+
+// ---- output delta + half-squared loss (phantom.py:169-182, training.py:59-71, 196-199) --------
+__global__ void output_delta_kernel(bool f32, int rows, int cols, bool relu, const void* y, int64_t ldy,
+                                    const void* t, int64_t ldt, const void* pre, int64_t ldp, void* d, int64_t ldd,
+                                    float scale, float loss_scale, float* loss) {
+  float acc = 0.f;
+  const int64_t n = (int64_t)rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    const float diff = ld_elem(y, r * ldy + c, f32) - ld_elem(t, r * ldt + c, f32);
+    acc += diff * diff;
+    const float g = relu ? (ld_elem(pre, r * ldp + c, f32) > 0.f ? 1.f : 0.f) : 1.f;
+    st_elem(d, r * ldd + c, f32, diff * g * scale);
+  }
+  for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  __shared__ float red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0 && loss) {
+    float s = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    atomicAdd(loss, s * loss_scale);
+  }
+}
+inline cudaError_t launch_output_delta(bool f32, int rows, int cols, bool relu, const void* y, int64_t ldy,
+                                       const void* t, int64_t ldt, const void* pre, int64_t ldp, void* d,
+                                       int64_t ldd, float scale, float loss_scale, float* loss, cudaStream_t st) {
+  output_delta_kernel<<<ew_grid((int64_t)rows * cols), 256, 0, st>>>(f32, rows, cols, relu, y, ldy, t, ldt, pre, ldp,
+                                                                      d, ldd, scale, loss_scale, loss);
+  return cudaGetLastError();
+}
+
+// ---- column sums (bias gradient, phantom.py:253): out[c] += sum_r x[r, c] --------------------
+__global__ void colsum_kernel(bool f32, int rows, int cols, const void* x, int64_t ld, float* out) {
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int ty = threadIdx.x >> 5;  // 8 row lanes
+  float acc = 0.f;
+  if (c < cols)
+    for (int r = blockIdx.y * 8 + ty; r < rows; r += gridDim.y * 8) acc += ld_elem(x, (int64_t)r * ld + c, f32);
+  __shared__ float red[8][33];
+  red[ty][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (ty == 0 && c < cols) {
+    float s = 0.f;
+    for (int i = 0; i < 8; ++i) s += red[i][threadIdx.x & 31];
+    atomicAdd(out + c, s);
+  }
+}
+inline cudaError_t launch_colsum(bool f32, int rows, int cols, const void* x, int64_t ld, float* out, int accumulate,
+                                 cudaStream_t st) {
+  if (!accumulate) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(float) * cols, st);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid((cols + 31) / 32, 1);
+  int ry = (rows + 255) / 256;
+  int maxy = (148 * 8 + (int)grid.x - 1) / (int)grid.x;
+  grid.y = ry < 1 ? 1 : (ry > maxy ? (maxy < 1 ? 1 : maxy) : ry);
+  colsum_kernel<<<grid, 256, 0, st>>>(f32, rows, cols, x, ld, out);
+  return cudaGetLastError();
+}
+
+// ---- SGD / Adam (training.py:74-82, 92-105) with non-finite detection -------------------------
+// hyper = [lr, beta1, beta2, eps, 1 - beta1^t, 1 - beta2^t]
+__global__ void optimizer_kernel(bool adam, const float* __restrict__ hyper, float* __restrict__ w,
+                                 const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v, int64_t n,
+                                 bool copy_f32, void* copy, int* bad) {
+  const float lr = hyper[0];
+  bool nonfinite = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    nonfinite |= !isfinite(gi);
+    float wi = w[i];
+    if (adam) {
+      const float b1 = hyper[1], b2 = hyper[2], eps = hyper[3], bc1 = hyper[4], bc2 = hyper[5];
+      const float mi = b1 * m[i] + (1.f - b1) * gi;
+      const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+      m[i] = mi;
+      v[i] = vi;
+      wi -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+    } else {
+      wi -= lr * gi;
+    }
+    w[i] = wi;
+    if (copy) st_elem(copy, i, copy_f32, wi);
+  }
+  if (bad && __any_sync(0xffffffffu, nonfinite) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+}
+inline cudaError_t launch_optimizer(bool adam, const float* hyper, float* w, const float* g, float* m, float* v,
+                                    int64_t n, bool copy_f32, void* copy, int* bad, cudaStream_t st) {
+  optimizer_kernel<<<ew_grid(n), 256, 0, st>>>(adam, hyper, w, g, m, v, n, copy_f32, copy, bad);
+  return cudaGetLastError();
+}
+
+// ---- casts and activations ------------------------------------------------------------------
+__global__ void cast_kernel(bool src_f32, const void* src, bool dst_f32, void* dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    st_elem(dst, i, dst_f32, ld_elem(src, i, src_f32));
+}
+inline cudaError_t launch_cast(bool src_f32, const void* src, bool dst_f32, void* dst, int64_t n, cudaStream_t st) {
+  cast_kernel<<<ew_grid(n), 256, 0, st>>>(src_f32, src, dst_f32, dst, n);
+  return cudaGetLastError();
+}
+
+__global__ void bias_act_kernel(bool f32, int rows, int cols, const void* x, int64_t ldx, const float* bias,
+                                bool relu, void* y, int64_t ldy) {
+  const int64_t n = (int64_t)rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    float v = ld_elem(x, r * ldx + c, f32) + (bias ? bias[c] : 0.f);
+    if (relu) v = fmaxf(v, 0.f);
+    st_elem(y, r * ldy + c, f32, v);
+  }
+}
+inline cudaError_t launch_bias_act(bool f32, int rows, int cols, const void* x, int64_t ldx, const float* bias,
+                                   bool relu, void* y, int64_t ldy, cudaStream_t st) {
+  bias_act_kernel<<<ew_grid((int64_t)rows * cols), 256, 0, st>>>(f32, rows, cols, x, ldx, bias, relu, y, ldy);
+  return cudaGetLastError();
+}
+
+__global__ void relu_mask_kernel(bool f32, int rows, int cols, void* x, int64_t ldx, const void* m, int64_t ldm) {
+  const int64_t n = (int64_t)rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    if (!(ld_elem(m, r * ldm + c, f32) > 0.f)) st_elem(x, r * ldx + c, f32, 0.f);
+  }
+}
+inline cudaError_t launch_relu_mask(bool f32, int rows, int cols, void* x, int64_t ldx, const void* m, int64_t ldm,
+                                    cudaStream_t st) {
+  relu_mask_kernel<<<ew_grid((int64_t)rows * cols), 256, 0, st>>>(f32, rows, cols, x, ldx, m, ldm);
+  return cudaGetLastError();
+}
+
+}  // namespace ppx

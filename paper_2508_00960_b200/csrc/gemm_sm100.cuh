@@ -1,0 +1,603 @@
+// Grouped, K-segmented tcgen05 GEMM for sm_100a with fused phantom-layer epilogues.
+//
+// One persistent kernel serves every dense contraction on the phantom-parallel hot path
+// (reference call sites phantom.py:152-264, tensor_parallel.py:115-145):
+//
+//   D[m, n] = sum_seg  A_seg[m, :] . B_seg[n, :]        (fp32 accumulation in TMEM)
+//
+// * Operands are staged by TMA (cp.async.bulk.tensor.3d, SWIZZLE_128B) into a 4-stage smem
+//   ring and consumed by tcgen05.mma issued from one thread; accumulators live in TMEM
+//   (2 x 256 columns, double buffered so the epilogue of tile i overlaps the MMAs of i+1).
+// * Each operand is either K-major or MN-major (the transposed-operand GEMMs of the backward
+//   pass read activations [batch, features] as MN-major tiles, no transpose kernels).
+// * A "problem" is one output matrix (or a stack of same-shaped blocks: the per-peer
+//   decompressor blocks); up to MAX_PROBS problems share one launch (grouped GEMM).
+// * A problem sums up to MAX_SEGS K-segments, each with its own tensor maps: this is how the
+//   local block and the (p-1) incoming phantom blocks become ONE K-concatenated contraction
+//   (phantom.py:152+156-157), how [delta | r] . [L ; C] is formed (phantom.py:228-229), and how
+//   the fp32 tier runs 3xTF32 (hi*hi + hi*lo + lo*hi) on the same machinery.
+// * Blocked coordinates: a segment's K range, or a problem's N range, can walk over "slots"
+//   (the third tensor-map dimension) skipping the caller's own rank, which reads the
+//   all-gathered phantom buffer [p, batch, k] directly (phantom.py:155-157, 202-205, 259-264).
+// * The epilogue fuses bias, ReLU, pre-activation store, the ReLU'-mask of the error
+//   recurrence, the output delta + half-squared loss, bias-gradient column sums, accumulate
+//   into an existing output, and in-place SGD / Adam on fp32 master weights.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace ppx {
+
+constexpr int BM = 128;           // tcgen05 M (cta_group::1)
+constexpr int BN_MAX = 256;       // max tcgen05 N per tile
+constexpr int STAGES = 4;         // smem ring depth
+constexpr int ROW_BYTES = 128;    // one SWIZZLE_128B row = one BK slice of K
+constexpr int A_STAGE_BYTES = BM * ROW_BYTES;          // 16 KB
+constexpr int B_STAGE_BYTES = BN_MAX * ROW_BYTES;      // 32 KB
+constexpr int NUM_THREADS = 256;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 spare, w4-7 epilogue
+constexpr int TMEM_COLS = 512;    // 2 accumulator stages x 256 fp32 columns
+constexpr int MAX_MAPS = 14;
+constexpr int MAX_PROBS = 4;
+constexpr int MAX_SEGS = 6;
+constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
+
+// epilogue flags
+enum : uint32_t {
+  EP_BIAS = 1u << 0,      // v += bias[col]
+  EP_RELU = 1u << 1,      // y = max(v, 0)
+  EP_PREACT = 1u << 2,    // store pre-activation (after bias) to `preact`
+  EP_MASK = 1u << 3,      // v *= (mask[row, col] > 0)   (ReLU'(preact) from the layer output)
+  EP_LOSS = 1u << 4,      // output layer: diff = y - target; aux = diff * act'(pre) * scale; loss += diff^2
+  EP_COLSUM = 1u << 5,    // colsum[col] += delta value (bias gradient, phantom.py:253)
+  EP_ACCUM = 1u << 6,     // out = out + v
+  EP_SGD = 1u << 7,       // master -= lr * v ; out = cast(master)
+  EP_ADAM = 1u << 8,      // Adam on master with m, v moments ; out = cast(master)
+  EP_GRAD = 1u << 9,      // also store the raw gradient to `aux` (fp32)
+  EP_FINITE = 1u << 10,   // flag non-finite accumulator values
+};
+
+struct Operand {
+  int8_t map;        // tensor-map index
+  int8_t mn;         // 0 = K-major, 1 = MN-major
+  int8_t slot_src;   // 0 = const, 1 = K-block index, 2 = N-block index
+  int8_t pad_;
+  int slot_base;
+  int slot_skip;     // raw slot index >= skip is shifted by one (own rank excluded); INT_MAX = none
+};
+
+struct Segment {
+  Operand a, b;
+  int k_tiles;       // number of BK slices
+  int kpb;           // BK slices per K block (K-blocked segments walk slots); == k_tiles otherwise
+  uint32_t idesc;    // tcgen05 instruction descriptor (majors, N, M)
+};
+
+struct Tensor2 {     // epilogue side tensor: row-major with leading dim, optional slot stride
+  void* ptr;
+  long long ld;
+  long long slot_stride;
+  int f32;           // 0 = bf16, 1 = fp32
+  int pad_;
+};
+
+struct Epilogue {
+  uint32_t flags;
+  int out_skip;      // N-block -> output slot skip (own rank)
+  Tensor2 out, aux, preact, mask, target, master, adam_m, adam_v;
+  const float* bias;
+  float* colsum;
+  float* loss;       // += sum diff^2 * loss_scale
+  int* bad;          // non-finite flag
+  const float* hyper;   // device scalars: [lr, beta1, beta2, eps, bias_corr1, bias_corr2]
+  float scale;       // delta scale (1 or 1/B)
+  float loss_scale;  // 0.5 or 0.5/B
+};
+
+struct Problem {
+  int M;             // rows of D
+  int nb_extent;     // columns per N block
+  int nblk;          // number of N blocks
+  int BN;            // tile N (multiple of 16, <= 256)
+  int m_tiles, npb;  // tiles along M, tiles per N block
+  int tile_begin;    // prefix over problems
+  int nsegs;
+  Segment segs[MAX_SEGS];
+  Epilogue epi;
+};
+
+struct alignas(64) GemmParams {
+  CUtensorMap maps[MAX_MAPS];
+  Problem probs[MAX_PROBS];
+  int nmaps;
+  int nprobs;
+  int total_tiles;
+};
+
+// ------------------------------------------------------------------------------------------
+// PTX helpers
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Blocking wait with a watchdog: a pipeline bug traps after ~20 s instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const uint64_t t0 = global_ns();
+  uint32_t n = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if ((++n & 0x3FFu) == 0 && global_ns() - t0 > 20000000000ull) asm volatile("trap;");
+  }
+}
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint32_t bar, uint32_t dst, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor (SWIZZLE_128B, version 1 for sm_100)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+  return d;
+}
+
+template <bool kTF32>
+__device__ __forceinline__ void mma_issue(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accum) {
+  if constexpr (kTF32) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+  } else {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+  }
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+        "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+        "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ------------------------------------------------------------------------------------------
+// epilogue element I/O (32 contiguous values of one row)
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void load32(const Tensor2& t, long long off, int nvalid, float* v) {
+  if (t.f32) {
+    const float* p = reinterpret_cast<const float*>(t.ptr) + off;
+    if (nvalid == 32 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4 q = reinterpret_cast<const float4*>(p)[i];
+        v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = i < nvalid ? p[i] : 0.f;
+    }
+  } else {
+    const __nv_bfloat16* p = reinterpret_cast<const __nv_bfloat16*>(t.ptr) + off;
+    if (nvalid == 32 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 q = reinterpret_cast<const uint4*>(p)[i];
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float2 f = __bfloat1622float2(h[j]);
+          v[8 * i + 2 * j] = f.x; v[8 * i + 2 * j + 1] = f.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = i < nvalid ? __bfloat162float(p[i]) : 0.f;
+    }
+  }
+}
+
+__device__ __forceinline__ void store32(const Tensor2& t, long long off, int nvalid, const float* v) {
+  if (t.f32) {
+    float* p = reinterpret_cast<float*>(t.ptr) + off;
+    if (nvalid == 32 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        reinterpret_cast<float4*>(p)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i < nvalid) p[i] = v[i];
+    }
+  } else {
+    __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(t.ptr) + off;
+    if (nvalid == 32 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 q;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(v[8 * i + 2 * j], v[8 * i + 2 * j + 1]);
+        reinterpret_cast<uint4*>(p)[i] = q;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i < nvalid) p[i] = __float2bfloat16_rn(v[i]);
+    }
+  }
+}
+
+// sum of v[i] over the 32 lanes of a warp; lane L returns the total for column L
+__device__ __forceinline__ float warp_transpose_sum(float* v, int lane) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < off; ++i) {
+      float send = up ? v[i] : v[i + off];
+      float keep = up ? v[i + off] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
+
+// ------------------------------------------------------------------------------------------
+// the kernel
+// ------------------------------------------------------------------------------------------
+struct TileCoord {
+  int prob, m0, qn, nin;
+};
+
+__device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, int t) {
+  int pi = 0;
+#pragma unroll 1
+  while (pi + 1 < P.nprobs && t >= P.probs[pi + 1].tile_begin) ++pi;
+  const Problem& pr = P.probs[pi];
+  int local = t - pr.tile_begin;
+  int ntn = pr.nblk * pr.npb;
+  int mt = local / ntn;
+  int nt = local - mt * ntn;
+  TileCoord c;
+  c.prob = pi;
+  c.m0 = mt * BM;
+  c.qn = nt / pr.npb;
+  c.nin = (nt - c.qn * pr.npb) * pr.BN;
+  return c;
+}
+
+__device__ __forceinline__ int op_slot(const Operand& o, int kblk, int qn) {
+  int raw = o.slot_src == 1 ? kblk : (o.slot_src == 2 ? qn : 0);
+  return o.slot_base + raw + (raw >= o.slot_skip ? 1 : 0);
+}
+
+template <bool kTF32>
+__global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t sA = base_u32;
+  const uint32_t sB = sA + STAGES * A_STAGE_BYTES;
+  const uint32_t sBar = sB + STAGES * B_STAGE_BYTES;
+  // barrier layout: full[STAGES], empty[STAGES], tfull[2], tempty[2], tmem addr slot
+  auto full_bar = [&](int s) { return sBar + 8u * s; };
+  auto empty_bar = [&](int s) { return sBar + 8u * (STAGES + s); };
+  auto tfull_bar = [&](int s) { return sBar + 8u * (2 * STAGES + s); };
+  auto tempty_bar = [&](int s) { return sBar + 8u * (2 * STAGES + 2 + s); };
+  const uint32_t tmem_slot = sBar + 8u * (2 * STAGES + 4);
+  uint8_t* smem_gen = smem_raw + (base_u32 - smem_u32(smem_raw));
+  volatile uint32_t* tmem_slot_ptr =
+      reinterpret_cast<volatile uint32_t*>(smem_gen + (tmem_slot - base_u32));
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  constexpr int ESIZE = kTF32 ? 4 : 2;
+  constexpr int BK = ROW_BYTES / ESIZE;     // elements of K per stage
+  constexpr int CH = ROW_BYTES / ESIZE;     // MN-major atom width in elements
+  constexpr int KMMA = 32 / ESIZE;          // K per tcgen05.mma
+  constexpr int NK = BK / KMMA;             // MMAs per stage (4)
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < P.nmaps; ++i) prefetch_map(&P.maps[i]);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(tfull_bar(s), 1);
+      mbar_init(tempty_bar(s), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot_ptr;
+
+  const int total = P.total_tiles;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        TileCoord tc = tile_coord(P, t);
+        const Problem& pr = P.probs[tc.prob];
+        const uint32_t bytes = (uint32_t)(BM + pr.BN) * ROW_BYTES;
+        for (int sg = 0; sg < pr.nsegs; ++sg) {
+          const Segment& seg = pr.segs[sg];
+          const CUtensorMap* ma = &P.maps[seg.a.map];
+          const CUtensorMap* mb = &P.maps[seg.b.map];
+          for (int kt = 0; kt < seg.k_tiles; ++kt) {
+            const int kblk = kt / seg.kpb;
+            const int kin = (kt - kblk * seg.kpb) * BK;
+            mbar_wait(empty_bar(stage), phase ^ 1u);
+            mbar_expect_tx(full_bar(stage), bytes);
+            const uint32_t da = sA + stage * A_STAGE_BYTES;
+            const uint32_t db = sB + stage * B_STAGE_BYTES;
+            const int slot_a = op_slot(seg.a, kblk, tc.qn);
+            const int slot_b = op_slot(seg.b, kblk, tc.qn);
+            if (!seg.a.mn) {
+              tma_load_3d(ma, full_bar(stage), da, kin, tc.m0, slot_a);
+            } else {
+#pragma unroll 1
+              for (int c = 0; c < BM / CH; ++c)
+                tma_load_3d(ma, full_bar(stage), da + c * (BK * ROW_BYTES), tc.m0 + c * CH, kin, slot_a);
+            }
+            if (!seg.b.mn) {
+              tma_load_3d(mb, full_bar(stage), db, kin, tc.nin, slot_b);
+            } else {
+#pragma unroll 1
+              for (int c = 0; c < pr.BN / CH; ++c)
+                tma_load_3d(mb, full_bar(stage), db + c * (BK * ROW_BYTES), tc.nin + c * CH, kin, slot_b);
+            }
+            if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int iter = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++iter) {
+        TileCoord tc = tile_coord(P, t);
+        const Problem& pr = P.probs[tc.prob];
+        const int as = iter & 1;
+        const uint32_t aphase = (iter >> 1) & 1;
+        mbar_wait(tempty_bar(as), aphase ^ 1u);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + as * BN_MAX;
+        uint32_t accum = 0;
+        for (int sg = 0; sg < pr.nsegs; ++sg) {
+          const Segment& seg = pr.segs[sg];
+          for (int kt = 0; kt < seg.k_tiles; ++kt) {
+            mbar_wait(full_bar(stage), phase);
+            tc_fence_after();
+            const uint32_t da = sA + stage * A_STAGE_BYTES;
+            const uint32_t db = sB + stage * B_STAGE_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < NK; ++kk) {
+              uint64_t ad = seg.a.mn ? sdesc(da + kk * (KMMA * ROW_BYTES), BK * ROW_BYTES, 1024)
+                                     : sdesc(da + kk * 32, 16, 1024);
+              uint64_t bd = seg.b.mn ? sdesc(db + kk * (KMMA * ROW_BYTES), BK * ROW_BYTES, 1024)
+                                     : sdesc(db + kk * 32, 16, 1024);
+              mma_issue<kTF32>(tmem_d, ad, bd, seg.idesc, accum);
+              accum = 1;
+            }
+            mma_commit(empty_bar(stage));
+            if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+          }
+        }
+        mma_commit(tfull_bar(as));
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ===================== epilogue =====================
+    const int wq = warp - 4;  // TMEM lane quadrant
+    int iter = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++iter) {
+      TileCoord tc = tile_coord(P, t);
+      const Problem& pr = P.probs[tc.prob];
+      const Epilogue& E = pr.epi;
+      const int as = iter & 1;
+      const uint32_t aphase = (iter >> 1) & 1;
+      mbar_wait(tfull_bar(as), aphase);
+      tc_fence_after();
+      const int row = tc.m0 + wq * 32 + lane;
+      const bool row_ok = row < pr.M;
+      const int oslot = tc.qn + (tc.qn >= E.out_skip ? 1 : 0);
+      const uint32_t flags = E.flags;
+      float loss_acc = 0.f;
+      bool bad = false;
+      const int nchunks = (pr.BN + 31) / 32;
+      for (int c = 0; c < nchunks; ++c) {
+        float v[32];
+        tmem_ld32(tmem_base + as * BN_MAX + c * 32 + ((uint32_t)(wq * 32) << 16), v);
+        const int col0 = tc.nin + c * 32;
+        int nvalid = pr.nb_extent - col0;
+        nvalid = nvalid > 32 ? 32 : nvalid;
+        const bool any = nvalid > 0;
+        if (flags & EP_FINITE) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) bad |= row_ok && (i < nvalid) && !isfinite(v[i]);
+        }
+        if (flags & EP_BIAS) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += (i < nvalid) ? E.bias[col0 + i] : 0.f;
+        }
+        const long long ooff = (long long)oslot * E.out.slot_stride + (long long)row * E.out.ld + col0;
+        if ((flags & EP_PREACT) && row_ok && any)
+          store32(E.preact, (long long)oslot * E.preact.slot_stride + (long long)row * E.preact.ld + col0, nvalid,
+                  v);
+        if (flags & (EP_SGD | EP_ADAM)) {
+          if (row_ok && any) {
+            if (flags & EP_GRAD)
+              store32(E.aux, (long long)oslot * E.aux.slot_stride + (long long)row * E.aux.ld + col0, nvalid, v);
+            const long long moff =
+                (long long)oslot * E.master.slot_stride + (long long)row * E.master.ld + col0;
+            float w[32];
+            load32(E.master, moff, nvalid, w);
+            const float lr = E.hyper[0];
+            if (flags & EP_ADAM) {
+              float m1[32], m2[32];
+              load32(E.adam_m, moff, nvalid, m1);
+              load32(E.adam_v, moff, nvalid, m2);
+              const float b1 = E.hyper[1], b2 = E.hyper[2], eps = E.hyper[3], bc1 = E.hyper[4], bc2 = E.hyper[5];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                m1[i] = b1 * m1[i] + (1.f - b1) * v[i];
+                m2[i] = b2 * m2[i] + (1.f - b2) * v[i] * v[i];
+                const float mh = m1[i] / bc1, vh = m2[i] / bc2;
+                w[i] -= lr * mh / (sqrtf(vh) + eps);
+              }
+              store32(E.adam_m, moff, nvalid, m1);
+              store32(E.adam_v, moff, nvalid, m2);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) w[i] -= lr * v[i];
+            }
+            store32(E.master, moff, nvalid, w);
+            if (E.out.ptr) store32(E.out, ooff, nvalid, w);
+          }
+        } else if (flags & EP_LOSS) {
+          float t[32], d[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) t[i] = 0.f;
+          if (row_ok && any) load32(E.target, (long long)row * E.target.ld + col0, nvalid, t);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const bool ok = row_ok && i < nvalid;
+            const float y = (flags & EP_RELU) ? fmaxf(v[i], 0.f) : v[i];
+            const float diff = ok ? (y - t[i]) : 0.f;
+            loss_acc += diff * diff;
+            const float g = (flags & EP_RELU) ? (v[i] > 0.f ? 1.f : 0.f) : 1.f;
+            d[i] = diff * g * E.scale;
+            v[i] = y;
+          }
+          if (row_ok && any) {
+            store32(E.out, ooff, nvalid, v);
+            store32(E.aux, (long long)row * E.aux.ld + col0, nvalid, d);
+          }
+          if (flags & EP_COLSUM) {
+            float s = warp_transpose_sum(d, lane);
+            if (lane < nvalid) atomicAdd(E.colsum + col0 + lane, s);
+          }
+        } else {
+          if (flags & EP_RELU) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+          }
+          if (flags & EP_MASK) {
+            float mk[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) mk[i] = 0.f;
+            if (row_ok && any) load32(E.mask, (long long)row * E.mask.ld + col0, nvalid, mk);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = (row_ok && i < nvalid && mk[i] > 0.f) ? v[i] : 0.f;
+          }
+          if (flags & EP_ACCUM) {
+            float o[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = 0.f;
+            if (row_ok && any) load32(E.out, ooff, nvalid, o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += (row_ok && i < nvalid) ? o[i] : 0.f;
+          }
+          if (row_ok && any) store32(E.out, ooff, nvalid, v);
+          if (flags & EP_COLSUM) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = (row_ok && i < nvalid) ? v[i] : 0.f;
+            float s = warp_transpose_sum(v, lane);
+            if (lane < nvalid) atomicAdd(E.colsum + col0 + lane, s);
+          }
+        }
+      }
+      if (flags & EP_LOSS) {
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) loss_acc += __shfl_xor_sync(0xffffffffu, loss_acc, off);
+        if (lane == 0) atomicAdd(E.loss, loss_acc * E.loss_scale);
+      }
+      if ((flags & EP_FINITE) && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(E.bad, 1);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_bar(as));
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+}  // namespace ppx

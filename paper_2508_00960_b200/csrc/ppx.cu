@@ -1,0 +1,727 @@
+// libppx.so — host side of the C ABI declared in include/ppx.h.
+//
+// Builds tensor maps and grouped-GEMM problem tables for the tcgen05 kernel in gemm_sm100.cuh,
+// launches the small elementwise kernels in elementwise.cuh, and drives NCCL for the phantom
+// all-gather / reduce-scatter.  No torch types cross this boundary.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <climits>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ppx.h"
+#include "elementwise.cuh"
+#include "gemm_sm100.cuh"
+
+struct ppx_ctx {
+  int world = 1, rank = 0, device = 0, num_sms = 148;
+  ncclComm_t comm = nullptr;
+  std::string err;
+  // FP32-tier hi/lo split workspace: a pool of chunks, bump-allocated per call and reused by the
+  // next call (stream ordered: FP32-tier calls of one ctx must share a stream)
+  std::vector<std::pair<char*, size_t>> ws;
+};
+
+namespace {
+
+using ppx::GemmParams;
+using ppx::Problem;
+using ppx::Segment;
+
+ppx_status fail(ppx_ctx* ctx, ppx_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  return st;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                  \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess) return fail(ctx, PPX_E_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define NCCL_TRY(ctx, expr)                                                                        \
+  do {                                                                                             \
+    ncclResult_t r_ = (expr);                                                                      \
+    if (r_ != ncclSuccess) return fail(ctx, PPX_E_PROTOCOL, "%s: %s", #expr, ncclGetErrorString(r_)); \
+  } while (0)
+
+inline int64_t round8(int64_t x) { return (x + 7) / 8 * 8; }
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+struct Flat {  // element offsets of the flat (rank, layer) parameter block
+  int64_t lds, ldk, local, comp, dec, bias, total;
+  Flat(int s, int k, int p) {
+    lds = round8(s);
+    ldk = round8(k);
+    local = 0;
+    comp = (int64_t)s * lds;
+    dec = comp + (int64_t)k * lds;
+    bias = dec + (int64_t)(p - 1) * s * ldk;
+    total = bias + round8(s);
+  }
+};
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+bool get_encode() {
+  std::call_once(g_encode_once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode != nullptr;
+}
+
+// 3D row-major view, in elements: [slots][rows][cols] with leading dim / slot stride
+struct View {
+  const void* ptr;
+  int64_t cols, rows, slots, ld, slot_stride;
+};
+inline View view2(const void* p, int64_t rows, int64_t cols, int64_t ld) { return {p, cols, rows, 1, ld, rows * ld}; }
+inline View view3(const void* p, int64_t slots, int64_t rows, int64_t cols, int64_t ld, int64_t ss) {
+  return {p, cols, rows, slots, ld, ss};
+}
+
+struct Opnd {
+  View v;
+  int mn = 0;         // 0 K-major (cols = K), 1 MN-major (cols = M or N)
+  int slot_src = 0;   // 0 const, 1 K-block, 2 N-block
+  int slot_base = 0;
+  int slot_skip = INT_MAX;
+};
+
+inline ppx::Tensor2 t2(void* p, int64_t ld, int f32, int64_t ss = 0) {
+  ppx::Tensor2 t;
+  t.ptr = p;
+  t.ld = ld;
+  t.slot_stride = ss;
+  t.f32 = f32;
+  t.pad_ = 0;
+  return t;
+}
+
+uint32_t make_idesc(bool tf32, int a_mn, int b_mn, int N) {
+  uint32_t d = 0;
+  d |= 1u << 4;                    // D = F32
+  d |= (tf32 ? 2u : 1u) << 7;      // A = TF32 / BF16
+  d |= (tf32 ? 2u : 1u) << 10;     // B = TF32 / BF16
+  d |= (uint32_t)(a_mn & 1) << 15;
+  d |= (uint32_t)(b_mn & 1) << 16;
+  d |= (uint32_t)(N >> 3) << 17;
+  d |= (uint32_t)(ppx::BM >> 4) << 24;
+  return d;
+}
+
+struct Builder {
+  ppx_ctx* ctx;
+  cudaStream_t st;
+  bool tf32;
+  int esize, BK, CH;
+  GemmParams P;
+  std::map<std::pair<const void*, int64_t>, std::pair<void*, void*>> splits;  // tf32 hi/lo copies
+  size_t ws_chunk = 0, ws_off = 0;
+  ppx_status status = PPX_OK;
+
+  void* ws_alloc(size_t bytes) {
+    while (ws_chunk < ctx->ws.size() && ws_off + bytes > ctx->ws[ws_chunk].second) {
+      ++ws_chunk;
+      ws_off = 0;
+    }
+    if (ws_chunk == ctx->ws.size()) {
+      size_t cap = bytes < ((size_t)64 << 20) ? ((size_t)64 << 20) : bytes;
+      char* p = nullptr;
+      if (cudaMalloc(&p, cap) != cudaSuccess) return nullptr;
+      ctx->ws.push_back({p, cap});
+      ws_off = 0;
+    }
+    void* r = ctx->ws[ws_chunk].first + ws_off;
+    ws_off += bytes;
+    return r;
+  }
+
+  Builder(ppx_ctx* c, ppx_dtype dt, void* stream) : ctx(c), st((cudaStream_t)stream), tf32(dt == PPX_FP32) {
+    esize = tf32 ? 4 : 2;
+    BK = ppx::ROW_BYTES / esize;
+    CH = BK;
+    memset(&P, 0, sizeof(P));
+  }
+
+  bool ok() const { return status == PPX_OK; }
+  void error(ppx_status s, const char* msg) {
+    if (status == PPX_OK) {
+      status = s;
+      fail(ctx, s, "%s", msg);
+    }
+  }
+
+  int add_map(const View& v, int box_inner, int box_rows) {
+    if (!ok()) return 0;
+    if (P.nmaps >= ppx::MAX_MAPS) { error(PPX_E_CONFIG, "too many tensor maps in one launch"); return 0; }
+    if (!get_encode()) { error(PPX_E_CUDA, "cuTensorMapEncodeTiled unavailable"); return 0; }
+    if ((reinterpret_cast<uintptr_t>(v.ptr) & 15) || (v.ld * esize) % 16 || (v.slot_stride * esize) % 16) {
+      error(PPX_E_CONFIG, "tensor base must be 16B aligned and leading dims multiples of 16 bytes");
+      return 0;
+    }
+    cuuint64_t dims[3] = {(cuuint64_t)v.cols, (cuuint64_t)v.rows, (cuuint64_t)v.slots};
+    cuuint64_t strides[2] = {(cuuint64_t)(v.ld * esize), (cuuint64_t)(v.slot_stride * esize)};
+    cuuint32_t box[3] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = g_encode(&P.maps[P.nmaps], tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                          3, const_cast<void*>(v.ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      char msg[256];
+      snprintf(msg, sizeof msg, "cuTensorMapEncodeTiled failed (%d): dims %llu,%llu,%llu box %d,%d", (int)r,
+               (unsigned long long)v.cols, (unsigned long long)v.rows, (unsigned long long)v.slots, box_inner,
+               box_rows);
+      error(PPX_E_CUDA, msg);
+      return 0;
+    }
+    return P.nmaps++;
+  }
+
+  // FP32 tier: hi = tf32-truncated x, lo = x - hi over the whole strided extent of the view.
+  // MN-major views are transposed while split and come back K-major (`mn` cleared).
+  std::pair<View, View> split(const View& v, int& mn) {
+    View hi = v, lo = v;
+    const int64_t n = (v.slots - 1) * v.slot_stride + (v.rows - 1) * v.ld + v.cols;
+    const bool tr = mn != 0;
+    auto key = std::make_pair(v.ptr, tr ? -n : n);
+    auto it = splits.find(key);
+    int64_t ldo = round8(v.rows), sso = v.cols * ldo;
+    void *h = nullptr, *l = nullptr;
+    if (it != splits.end()) {
+      h = it->second.first;
+      l = it->second.second;
+    } else {
+      size_t elems = tr ? (size_t)(v.slots * sso) : (size_t)n;
+      size_t bytes = (elems * 4 + 255) / 256 * 256;
+      h = ws_alloc(bytes);
+      l = ws_alloc(bytes);
+      if (!h || !l) { error(PPX_E_CUDA, "workspace allocation failed"); return {hi, lo}; }
+      if (tr)
+        ppx::launch_split_tf32_t(reinterpret_cast<const float*>(v.ptr), (int)v.slots, (int)v.rows, (int)v.cols, v.ld,
+                                 v.slot_stride, (float*)h, (float*)l, ldo, sso, st);
+      else
+        ppx::launch_split_tf32(reinterpret_cast<const float*>(v.ptr), (float*)h, (float*)l, n, st);
+      splits[key] = {h, l};
+    }
+    if (tr) {
+      hi = View{h, v.rows, v.cols, v.slots, ldo, sso};
+      lo = View{l, v.rows, v.cols, v.slots, ldo, sso};
+      mn = 0;
+    } else {
+      hi.ptr = h;
+      lo.ptr = l;
+    }
+    return {hi, lo};
+  }
+
+  Problem* new_problem(int M, int nb_extent, int nblk, bool b_mn) {
+    if (!ok()) return nullptr;
+    if (P.nprobs >= ppx::MAX_PROBS) { error(PPX_E_CONFIG, "too many problems in one launch"); return nullptr; }
+    if (M <= 0 || nb_extent <= 0 || nblk <= 0) { error(PPX_E_CONFIG, "empty GEMM problem"); return nullptr; }
+    Problem* pr = &P.probs[P.nprobs++];
+    memset(pr, 0, sizeof(*pr));
+    const int gran = b_mn ? CH : 16;
+    int ntiles = (int)cdiv(nb_extent, ppx::BN_MAX);
+    int bn = (int)cdiv(cdiv(nb_extent, ntiles), gran) * gran;
+    if (bn > ppx::BN_MAX) bn = ppx::BN_MAX;
+    pr->M = M;
+    pr->nb_extent = nb_extent;
+    pr->nblk = nblk;
+    pr->BN = bn;
+    pr->m_tiles = (int)cdiv(M, ppx::BM);
+    pr->npb = (int)cdiv(nb_extent, bn);
+    pr->epi.out_skip = INT_MAX;
+    return pr;
+  }
+
+  void add_segment(Problem* pr, Opnd a, Opnd b, int k_tiles, int kpb) {
+    if (!ok() || !pr) return;
+    if (k_tiles <= 0) { error(PPX_E_CONFIG, "empty K segment"); return; }
+    auto push = [&](const View& av, const View& bv) {
+      if (pr->nsegs >= ppx::MAX_SEGS) { error(PPX_E_CONFIG, "too many K segments"); return; }
+      Segment& s = pr->segs[pr->nsegs++];
+      s.a.map = (int8_t)(a.mn ? add_map(av, CH, BK) : add_map(av, BK, ppx::BM));
+      s.a.mn = (int8_t)a.mn;
+      s.a.slot_src = (int8_t)a.slot_src;
+      s.a.slot_base = a.slot_base;
+      s.a.slot_skip = a.slot_skip;
+      s.b.map = (int8_t)(b.mn ? add_map(bv, CH, BK) : add_map(bv, BK, pr->BN));
+      s.b.mn = (int8_t)b.mn;
+      s.b.slot_src = (int8_t)b.slot_src;
+      s.b.slot_base = b.slot_base;
+      s.b.slot_skip = b.slot_skip;
+      s.k_tiles = k_tiles;
+      s.kpb = kpb;
+      s.idesc = make_idesc(tf32, a.mn, b.mn, pr->BN);
+    };
+    if (!tf32) {
+      push(a.v, b.v);
+    } else {
+      auto as = split(a.v, a.mn);
+      auto bs = split(b.v, b.mn);
+      if (!ok()) return;
+      push(as.second, bs.first);  // lo * hi
+      push(as.first, bs.second);  // hi * lo
+      push(as.first, bs.first);   // hi * hi
+    }
+  }
+
+  ppx_status launch() {
+    if (!ok()) return status;
+    int tiles = 0;
+    for (int i = 0; i < P.nprobs; ++i) {
+      P.probs[i].tile_begin = tiles;
+      tiles += P.probs[i].m_tiles * P.probs[i].nblk * P.probs[i].npb;
+    }
+    P.total_tiles = tiles;
+    if (tiles == 0) return PPX_OK;
+    int grid = tiles < ctx->num_sms ? tiles : ctx->num_sms;
+    cudaError_t e = tf32 ? ppx::launch_gemm<true>(P, grid, st) : ppx::launch_gemm<false>(P, grid, st);
+    if (e != cudaSuccess) return fail(ctx, PPX_E_CUDA, "gemm launch: %s", cudaGetErrorString(e));
+    return PPX_OK;
+  }
+};
+
+inline bool bad_layer(const ppx_layer* L) {
+  return !L || L->s < 1 || L->k < 1 || L->k > L->s || L->p < 1 || L->rank < 0 || L->rank >= L->p || !L->w ||
+         !L->master;
+}
+
+inline const char* elem(ppx_dtype dt, const void* base, int64_t off) {
+  return reinterpret_cast<const char*>(base) + off * (dt == PPX_FP32 ? 4 : 2);
+}
+
+}  // namespace
+
+namespace ppx {
+template <bool kTF32>
+cudaError_t launch_gemm(const GemmParams& P, int grid, cudaStream_t st) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  gemm_kernel<kTF32><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(P);
+  return cudaGetLastError();
+}
+template cudaError_t launch_gemm<true>(const GemmParams&, int, cudaStream_t);
+template cudaError_t launch_gemm<false>(const GemmParams&, int, cudaStream_t);
+}  // namespace ppx
+
+// =============================================================================================
+// C ABI
+// =============================================================================================
+extern "C" {
+
+int ppx_abi_version(void) { return PPX_ABI_VERSION; }
+
+int64_t ppx_layer_elems(int32_t s, int32_t k, int32_t p) { return Flat(s, k, p).total; }
+
+ppx_status ppx_get_unique_id(uint8_t uid[128]) {
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return PPX_E_PROTOCOL;
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  memcpy(uid, &id, 128);
+  return PPX_OK;
+}
+
+ppx_status ppx_create(int32_t world, int32_t rank, int32_t device, const uint8_t* uid, ppx_ctx** out) {
+  if (!out || world < 1 || rank < 0 || rank >= world) return PPX_E_CONFIG;
+  ppx_ctx* ctx = new ppx_ctx();
+  ctx->world = world;
+  ctx->rank = rank;
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) { delete ctx; return PPX_E_CUDA; }
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0) ctx->num_sms = sms;
+  if (world > 1) {
+    if (!uid) { delete ctx; return PPX_E_CONFIG; }
+    ncclUniqueId id;
+    memcpy(&id, uid, 128);
+    if (ncclCommInitRank(&ctx->comm, world, id, rank) != ncclSuccess) { delete ctx; return PPX_E_PROTOCOL; }
+  }
+  *out = ctx;
+  return PPX_OK;
+}
+
+ppx_status ppx_destroy(ppx_ctx* ctx) {
+  if (!ctx) return PPX_OK;
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  for (auto& c : ctx->ws) cudaFree(c.first);
+  delete ctx;
+  return PPX_OK;
+}
+
+const char* ppx_last_error(const ppx_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+int32_t ppx_num_sms(const ppx_ctx* ctx) { return ctx ? ctx->num_sms : 0; }
+
+// ---------------------------------------------------------------------------------------------
+ppx_status ppx_compress(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, const void* y_prev, int64_t ld_y,
+                        void* phantoms, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (bad_layer(L) || B < 1 || !y_prev || !phantoms) return fail(ctx, PPX_E_CONFIG, "ppx_compress: bad arguments");
+  Flat f(L->s, L->k, L->p);
+  Builder b(ctx, dt, stream);
+  Problem* pr = b.new_problem(B, L->k, 1, false);
+  Opnd a{view2(y_prev, B, L->s, ld_y)};
+  Opnd w{view2(elem(dt, L->w, f.comp), L->k, L->s, f.lds)};
+  b.add_segment(pr, a, w, (int)cdiv(L->s, b.BK), (int)cdiv(L->s, b.BK));
+  if (pr) pr->epi.out = t2((char*)phantoms + (int64_t)L->rank * B * f.ldk * b.esize, f.ldk, dt == PPX_FP32);
+  return b.launch();
+}
+
+static ppx_status forward_common(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, ppx_act act,
+                                 const void* y_prev, int64_t ld_y, const void* phantoms, void* stream, Builder& b,
+                                 Problem*& pr) {
+  Flat f(L->s, L->k, L->p);
+  pr = b.new_problem(B, L->s, 1, false);
+  Opnd a{view2(y_prev, B, L->s, ld_y)};
+  Opnd w{view2(elem(dt, L->w, f.local), L->s, L->s, f.lds)};
+  b.add_segment(pr, a, w, (int)cdiv(L->s, b.BK), (int)cdiv(L->s, b.BK));
+  if (L->p > 1) {
+    if (!phantoms) return fail(ctx, PPX_E_SEQUENCING, "forward: phantom buffer missing");
+    Opnd g{view3(phantoms, L->p, B, L->k, f.ldk, (int64_t)B * f.ldk)};
+    g.slot_src = 1;
+    g.slot_skip = L->rank;
+    Opnd d{view3(elem(dt, L->w, f.dec), L->p - 1, L->s, L->k, f.ldk, (int64_t)L->s * f.ldk)};
+    d.slot_src = 1;
+    int kpb = (int)cdiv(L->k, b.BK);
+    b.add_segment(pr, g, d, kpb * (L->p - 1), kpb);
+  }
+  if (pr) {
+    pr->epi.bias = L->master + f.bias;
+    pr->epi.flags = ppx::EP_BIAS | (act == PPX_RELU ? ppx::EP_RELU : 0u);
+  }
+  return b.ok() ? PPX_OK : b.status;
+}
+
+ppx_status ppx_forward_update(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, ppx_act act,
+                              const void* y_prev, int64_t ld_y, const void* phantoms, void* y_out, int64_t ld_out,
+                              void* preact, int64_t ld_pre, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (bad_layer(L) || B < 1 || !y_prev || !y_out) return fail(ctx, PPX_E_CONFIG, "ppx_forward_update: bad arguments");
+  Builder b(ctx, dt, stream);
+  Problem* pr = nullptr;
+  ppx_status s = forward_common(ctx, dt, L, B, act, y_prev, ld_y, phantoms, stream, b, pr);
+  if (s != PPX_OK) return s;
+  const int f32 = dt == PPX_FP32;
+  pr->epi.out = t2(y_out, ld_out, f32);
+  if (preact) {
+    pr->epi.flags |= ppx::EP_PREACT;
+    pr->epi.preact = t2(preact, ld_pre, f32);
+  }
+  return b.launch();
+}
+
+ppx_status ppx_forward_output(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, ppx_act act,
+                              const void* y_prev, int64_t ld_y, const void* phantoms, void* y_out, int64_t ld_out,
+                              const void* target, int64_t ld_t, void* delta, int64_t ld_d, float delta_scale,
+                              float loss_scale, float* loss, float* bias_grad, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (bad_layer(L) || B < 1 || !y_prev || !y_out || !target || !delta || !loss)
+    return fail(ctx, PPX_E_CONFIG, "ppx_forward_output: bad arguments");
+  Builder b(ctx, dt, stream);
+  Problem* pr = nullptr;
+  ppx_status s = forward_common(ctx, dt, L, B, act, y_prev, ld_y, phantoms, stream, b, pr);
+  if (s != PPX_OK) return s;
+  const int f32 = dt == PPX_FP32;
+  pr->epi.flags |= ppx::EP_LOSS | (bias_grad ? ppx::EP_COLSUM : 0u);
+  pr->epi.out = t2(y_out, ld_out, f32);
+  pr->epi.aux = t2(delta, ld_d, f32);
+  pr->epi.target = t2(const_cast<void*>(target), ld_t, f32);
+  pr->epi.scale = delta_scale;
+  pr->epi.loss_scale = loss_scale;
+  pr->epi.loss = loss;
+  pr->epi.colsum = bias_grad;
+  return b.launch();
+}
+
+ppx_status ppx_output_delta(ppx_ctx* ctx, ppx_dtype dt, int32_t B, int32_t s, ppx_act act, const void* y_out,
+                            int64_t ld_y, const void* target, int64_t ld_t, const void* pre, int64_t ld_p, void* delta,
+                            int64_t ld_d, float delta_scale, float loss_scale, float* loss, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (B < 1 || s < 1 || !y_out || !target || !delta || (act == PPX_RELU && !pre))
+    return fail(ctx, PPX_E_CONFIG, "ppx_output_delta: bad arguments");
+  cudaError_t e = ppx::launch_output_delta(dt == PPX_FP32, B, s, act == PPX_RELU, y_out, ld_y, target, ld_t, pre, ld_p,
+                                           delta, ld_d, delta_scale, loss_scale, loss, (cudaStream_t)stream);
+  return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "output_delta: %s", cudaGetErrorString(e));
+}
+
+ppx_status ppx_error_phantoms(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, const void* delta,
+                              int64_t ld_d, void* contrib, int32_t accumulate, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (bad_layer(L) || B < 1 || !delta || !contrib) return fail(ctx, PPX_E_CONFIG, "ppx_error_phantoms: bad arguments");
+  if (L->p < 2) return PPX_OK;  // no peers: every slot but the (unwritten) own one is absent
+  Flat f(L->s, L->k, L->p);
+  Builder b(ctx, dt, stream);
+  Problem* pr = b.new_problem(B, L->k, L->p - 1, true);
+  Opnd a{view2(delta, B, L->s, ld_d)};
+  Opnd d{view3(elem(dt, L->w, f.dec), L->p - 1, L->s, L->k, f.ldk, (int64_t)L->s * f.ldk)};
+  d.mn = 1;
+  d.slot_src = 2;
+  int kt = (int)cdiv(L->s, b.BK);
+  b.add_segment(pr, a, d, kt, kt);
+  if (pr) {
+    pr->epi.out = t2(contrib, f.ldk, dt == PPX_FP32, (int64_t)B * f.ldk);
+    pr->epi.out_skip = L->rank;
+    pr->epi.flags = accumulate ? ppx::EP_ACCUM : 0u;
+  }
+  return b.launch();
+}
+
+static ncclDataType_t nccl_type(ppx_dtype dt) { return dt == PPX_FP32 ? ncclFloat32 : ncclBfloat16; }
+
+ppx_status ppx_all_gather(ppx_ctx* ctx, ppx_dtype dt, void* phantoms, int64_t slot_elems, int32_t local_ranks,
+                          void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (ctx->world == 1) return PPX_OK;
+  const int64_t chunk = slot_elems * local_ranks;
+  char* base = (char*)phantoms;
+  const int es = dt == PPX_FP32 ? 4 : 2;
+  NCCL_TRY(ctx, ncclAllGather(base + (int64_t)ctx->rank * chunk * es, base, (size_t)chunk, nccl_type(dt), ctx->comm,
+                              (cudaStream_t)stream));
+  return PPX_OK;
+}
+
+ppx_status ppx_reduce_scatter(ppx_ctx* ctx, ppx_dtype dt, void* contrib, int64_t slot_elems, int32_t local_ranks,
+                              void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (ctx->world == 1) return PPX_OK;
+  const int64_t chunk = slot_elems * local_ranks;
+  char* base = (char*)contrib;
+  const int es = dt == PPX_FP32 ? 4 : 2;
+  NCCL_TRY(ctx, ncclReduceScatter(base, base + (int64_t)ctx->rank * chunk * es, (size_t)chunk, nccl_type(dt), ncclSum,
+                                  ctx->comm, (cudaStream_t)stream));
+  return PPX_OK;
+}
+
+ppx_status ppx_all_reduce_f32(ppx_ctx* ctx, float* buf, int64_t count, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (ctx->world == 1) return PPX_OK;
+  NCCL_TRY(ctx, ncclAllReduce(buf, buf, (size_t)count, ncclFloat32, ncclSum, ctx->comm, (cudaStream_t)stream));
+  return PPX_OK;
+}
+
+ppx_status ppx_all_reduce(ppx_ctx* ctx, ppx_dtype dt, void* buf, int64_t count, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (ctx->world == 1) return PPX_OK;
+  NCCL_TRY(ctx, ncclAllReduce(buf, buf, (size_t)count, nccl_type(dt), ncclSum, ctx->comm, (cudaStream_t)stream));
+  return PPX_OK;
+}
+
+static void set_update(ppx::Epilogue& E, const ppx_update* upd, ppx_dtype dt, int64_t off, int64_t ld, int64_t ss) {
+  const int es = dt == PPX_FP32 ? 4 : 2;
+  E.flags = (upd->kind == PPX_UPDATE_ADAM ? ppx::EP_ADAM : ppx::EP_SGD) | (upd->bad ? ppx::EP_FINITE : 0u);
+  E.hyper = upd->hyper;
+  E.master = t2(upd->master + off, ld, 1, ss);
+  if (upd->kind == PPX_UPDATE_ADAM) {
+    E.adam_m = t2(upd->adam_m + off, ld, 1, ss);
+    E.adam_v = t2(upd->adam_v + off, ld, 1, ss);
+  }
+  E.out = t2(upd->w_next ? (char*)upd->w_next + off * es : nullptr, ld, dt == PPX_FP32, ss);
+  if (upd->grad) {
+    E.flags |= ppx::EP_GRAD;
+    E.aux = t2(upd->grad + off, ld, 1, ss);
+  }
+  E.bad = upd->bad;
+}
+
+ppx_status ppx_param_grads(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, const void* delta,
+                           int64_t ld_d, const void* y_prev, int64_t ld_y, const void* phantoms,
+                           const void* received, float* grad, const ppx_update* upd, int32_t with_bias,
+                           void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  const bool update = upd && upd->kind != PPX_UPDATE_NONE;
+  if (bad_layer(L) || B < 1 || !delta || !y_prev || (!grad && !update))
+    return fail(ctx, PPX_E_CONFIG, "ppx_param_grads: bad arguments");
+  if (update && (!upd->master || !upd->hyper || (upd->kind == PPX_UPDATE_ADAM && (!upd->adam_m || !upd->adam_v))))
+    return fail(ctx, PPX_E_CONFIG, "ppx_param_grads: incomplete update");
+  if (L->p > 1 && (!phantoms || !received))
+    return fail(ctx, PPX_E_SEQUENCING, "ppx_param_grads: phantom tape or received gradient missing");
+  Flat f(L->s, L->k, L->p);
+  Builder b(ctx, dt, stream);
+  const int kt = (int)cdiv(B, b.BK);
+  // d local = delta^T y_prev   [s, s]
+  {
+    Problem* pr = b.new_problem(L->s, L->s, 1, true);
+    Opnd a{view2(delta, B, L->s, ld_d)};
+    a.mn = 1;
+    Opnd y{view2(y_prev, B, L->s, ld_y)};
+    y.mn = 1;
+    b.add_segment(pr, a, y, kt, kt);
+    if (pr) {
+      if (update) set_update(pr->epi, upd, dt, f.local, f.lds, 0);
+      else pr->epi.out = t2(grad + f.local, f.lds, 1);
+    }
+  }
+  // d compressor = r^T y_prev   [k, s]   (r is zero when p == 1: skip, gradient is zero)
+  if (L->p > 1) {
+    Problem* pr = b.new_problem(L->k, L->s, 1, true);
+    Opnd r{view2(received, B, L->k, f.ldk)};
+    r.mn = 1;
+    Opnd y{view2(y_prev, B, L->s, ld_y)};
+    y.mn = 1;
+    b.add_segment(pr, r, y, kt, kt);
+    if (pr) {
+      if (update) set_update(pr->epi, upd, dt, f.comp, f.lds, 0);
+      else pr->epi.out = t2(grad + f.comp, f.lds, 1);
+    }
+    // d decompressor_q = delta^T g_{src(q)}   [p-1][s, k]
+    Problem* pd = b.new_problem(L->s, L->k, L->p - 1, true);
+    Opnd a{view2(delta, B, L->s, ld_d)};
+    a.mn = 1;
+    Opnd g{view3(phantoms, L->p, B, L->k, f.ldk, (int64_t)B * f.ldk)};
+    g.mn = 1;
+    g.slot_src = 2;
+    g.slot_skip = L->rank;
+    b.add_segment(pd, a, g, kt, kt);
+    if (pd) {
+      if (update) set_update(pd->epi, upd, dt, f.dec, f.ldk, (int64_t)L->s * f.ldk);
+      else pd->epi.out = t2(grad + f.dec, f.ldk, 1, (int64_t)L->s * f.ldk);
+    }
+  } else if (grad) {
+    cudaMemsetAsync(grad + f.comp, 0, sizeof(float) * L->k * f.lds, (cudaStream_t)stream);
+  }
+  ppx_status s = b.launch();
+  if (s != PPX_OK) return s;
+  if (with_bias && grad) {
+    cudaError_t e = ppx::launch_colsum(dt == PPX_FP32, B, L->s, delta, ld_d, grad + f.bias, 0, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(ctx, PPX_E_CUDA, "colsum: %s", cudaGetErrorString(e));
+  }
+  return PPX_OK;
+}
+
+ppx_status ppx_backward_delta(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, ppx_act act_prev,
+                              const void* delta, int64_t ld_d, const void* received, const void* mask_src,
+                              int64_t ld_m, void* delta_prev, int64_t ld_dp, float* bias_grad_prev, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (bad_layer(L) || B < 1 || !delta || !delta_prev || (act_prev == PPX_RELU && !mask_src))
+    return fail(ctx, PPX_E_CONFIG, "ppx_backward_delta: bad arguments");
+  if (L->p > 1 && !received) return fail(ctx, PPX_E_SEQUENCING, "ppx_backward_delta: received gradient missing");
+  Flat f(L->s, L->k, L->p);
+  Builder b(ctx, dt, stream);
+  Problem* pr = b.new_problem(B, L->s, 1, true);
+  Opnd a{view2(delta, B, L->s, ld_d)};
+  Opnd w{view2(elem(dt, L->w, f.local), L->s, L->s, f.lds)};
+  w.mn = 1;
+  b.add_segment(pr, a, w, (int)cdiv(L->s, b.BK), (int)cdiv(L->s, b.BK));
+  if (L->p > 1) {
+    Opnd r{view2(received, B, L->k, f.ldk)};
+    Opnd c{view2(elem(dt, L->w, f.comp), L->k, L->s, f.lds)};
+    c.mn = 1;
+    b.add_segment(pr, r, c, (int)cdiv(L->k, b.BK), (int)cdiv(L->k, b.BK));
+  }
+  if (pr) {
+    const int f32 = dt == PPX_FP32;
+    pr->epi.out = t2(delta_prev, ld_dp, f32);
+    if (act_prev == PPX_RELU) {
+      pr->epi.flags |= ppx::EP_MASK;
+      pr->epi.mask = t2(const_cast<void*>(mask_src), ld_m, f32);
+    }
+    if (bias_grad_prev) {
+      pr->epi.flags |= ppx::EP_COLSUM;
+      pr->epi.colsum = bias_grad_prev;
+    }
+  }
+  return b.launch();
+}
+
+ppx_status ppx_colsum(ppx_ctx* ctx, ppx_dtype dt, int32_t rows, int32_t cols, const void* x, int64_t ld, float* out,
+                      int32_t accumulate, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (rows < 1 || cols < 1 || !x || !out) return fail(ctx, PPX_E_CONFIG, "ppx_colsum: bad arguments");
+  cudaError_t e = ppx::launch_colsum(dt == PPX_FP32, rows, cols, x, ld, out, accumulate, (cudaStream_t)stream);
+  return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "colsum: %s", cudaGetErrorString(e));
+}
+
+ppx_status ppx_optimizer_step(ppx_ctx* ctx, int32_t kind, const float* hyper, float* params, const float* grad,
+                              float* adam_m, float* adam_v, int64_t n, ppx_dtype dt, void* w_copy, int* bad,
+                              void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (n < 0 || !hyper || (n > 0 && (!params || !grad)) ||
+      (kind == PPX_UPDATE_ADAM && n > 0 && (!adam_m || !adam_v)) ||
+      (kind != PPX_UPDATE_SGD && kind != PPX_UPDATE_ADAM))
+    return fail(ctx, PPX_E_CONFIG, "ppx_optimizer_step: bad arguments");
+  if (n == 0) return PPX_OK;
+  cudaError_t e = ppx::launch_optimizer(kind == PPX_UPDATE_ADAM, hyper, params, grad, adam_m, adam_v, n,
+                                        dt == PPX_FP32, w_copy, bad, (cudaStream_t)stream);
+  return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "optimizer: %s", cudaGetErrorString(e));
+}
+
+ppx_status ppx_gemm(ppx_ctx* ctx, ppx_dtype dt, int32_t M, int32_t N, int32_t K, const void* a, int64_t lda,
+                    int32_t trans_a, const void* bm, int64_t ldb, int32_t trans_b, void* c, int64_t ldc,
+                    ppx_dtype out_dt, const ppx_epilogue* epi, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (M < 1 || N < 1 || K < 1 || !a || !bm || !c) return fail(ctx, PPX_E_CONFIG, "ppx_gemm: bad arguments");
+  Builder b(ctx, dt, stream);
+  const bool b_mn = !trans_b;
+  Problem* pr = b.new_problem(M, N, 1, b_mn);
+  Opnd A{trans_a ? view2(a, K, M, lda) : view2(a, M, K, lda)};
+  A.mn = trans_a ? 1 : 0;
+  Opnd Bo{trans_b ? view2(bm, N, K, ldb) : view2(bm, K, N, ldb)};
+  Bo.mn = b_mn ? 1 : 0;
+  int kt = (int)cdiv(K, b.BK);
+  b.add_segment(pr, A, Bo, kt, kt);
+  if (pr) {
+    const int f32 = out_dt == PPX_FP32;
+    pr->epi.out = t2(c, ldc, f32);
+    if (epi) {
+      if (epi->bias) { pr->epi.flags |= ppx::EP_BIAS; pr->epi.bias = epi->bias; }
+      if (epi->act == PPX_RELU) pr->epi.flags |= ppx::EP_RELU;
+      if (epi->accumulate) pr->epi.flags |= ppx::EP_ACCUM;
+      if (epi->mask) { pr->epi.flags |= ppx::EP_MASK; pr->epi.mask = t2(const_cast<void*>(epi->mask), epi->ld_mask, f32); }
+      if (epi->colsum) { pr->epi.flags |= ppx::EP_COLSUM; pr->epi.colsum = epi->colsum; }
+    }
+  }
+  return b.launch();
+}
+
+ppx_status ppx_cast(ppx_ctx* ctx, ppx_dtype src_dt, const void* src, ppx_dtype dst_dt, void* dst, int64_t n,
+                    void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (n < 0 || (n > 0 && (!src || !dst))) return fail(ctx, PPX_E_CONFIG, "ppx_cast: bad arguments");
+  if (n == 0) return PPX_OK;
+  cudaError_t e = ppx::launch_cast(src_dt == PPX_FP32, src, dst_dt == PPX_FP32, dst, n, (cudaStream_t)stream);
+  return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "cast: %s", cudaGetErrorString(e));
+}
+
+ppx_status ppx_bias_act(ppx_ctx* ctx, ppx_dtype dt, int32_t rows, int32_t cols, const void* x, int64_t ldx,
+                        const float* bias, ppx_act act, void* y, int64_t ldy, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (rows < 1 || cols < 1 || !x || !y) return fail(ctx, PPX_E_CONFIG, "ppx_bias_act: bad arguments");
+  cudaError_t e = ppx::launch_bias_act(dt == PPX_FP32, rows, cols, x, ldx, bias, act == PPX_RELU, y, ldy,
+                                       (cudaStream_t)stream);
+  return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "bias_act: %s", cudaGetErrorString(e));
+}
+
+ppx_status ppx_relu_mask(ppx_ctx* ctx, ppx_dtype dt, int32_t rows, int32_t cols, void* x, int64_t ldx,
+                         const void* mask_src, int64_t ldm, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (rows < 1 || cols < 1 || !x || !mask_src) return fail(ctx, PPX_E_CONFIG, "ppx_relu_mask: bad arguments");
+  cudaError_t e = ppx::launch_relu_mask(dt == PPX_FP32, rows, cols, x, ldx, mask_src, ldm, (cudaStream_t)stream);
+  return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "relu_mask: %s", cudaGetErrorString(e));
+}
+
+}  // extern "C"
