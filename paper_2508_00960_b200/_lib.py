@@ -159,16 +159,19 @@ class Context:
             pass
 
 
-_default: dict[int, Context] = {}
+_tls = threading.local()
 
 
 def default_context(device: int = 0) -> Context:
-    """Single-GPU context (world = 1) shared by the in-process API on `device`."""
-    with _lock:
-        ctx = _default.get(device)
+    """Single-GPU context (world = 1) for the in-process API on `device`.
+
+    A ppx_ctx is not re-entrant (it owns the FP32-tier workspace and the last-error string), and
+    the in-process Communicator runs one host thread per logical rank, so contexts are per
+    (thread, device)."""
+    cache = getattr(_tls, "ctxs", None)
+    if cache is None:
+        cache = _tls.ctxs = {}
+    ctx = cache.get(device)
     if ctx is None:
-        ctx = Context(1, 0, device)
-        with _lock:
-            _default.setdefault(device, ctx)
-            ctx = _default[device]
+        ctx = cache[device] = Context(1, 0, device)
     return ctx

@@ -16,6 +16,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/ppx.h"
@@ -171,8 +172,22 @@ struct Builder {
     }
   }
 
+  struct MapKey {
+    const void* ptr;
+    int64_t cols, rows, slots, ld, ss;
+    int bi, br;
+    bool operator<(const MapKey& o) const {
+      return std::tie(ptr, cols, rows, slots, ld, ss, bi, br) <
+             std::tie(o.ptr, o.cols, o.rows, o.slots, o.ld, o.ss, o.bi, o.br);
+    }
+  };
+  std::map<MapKey, int> map_cache;
+
   int add_map(const View& v, int box_inner, int box_rows) {
     if (!ok()) return 0;
+    MapKey key{v.ptr, v.cols, v.rows, v.slots, v.ld, v.slot_stride, box_inner, box_rows};
+    auto hit = map_cache.find(key);
+    if (hit != map_cache.end()) return hit->second;
     if (P.nmaps >= ppx::MAX_MAPS) { error(PPX_E_CONFIG, "too many tensor maps in one launch"); return 0; }
     if (!get_encode()) { error(PPX_E_CUDA, "cuTensorMapEncodeTiled unavailable"); return 0; }
     if ((reinterpret_cast<uintptr_t>(v.ptr) & 15) || (v.ld * esize) % 16 || (v.slot_stride * esize) % 16) {
@@ -195,6 +210,7 @@ struct Builder {
       error(PPX_E_CUDA, msg);
       return 0;
     }
+    map_cache[key] = P.nmaps;
     return P.nmaps++;
   }
 
