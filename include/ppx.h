@@ -66,8 +66,12 @@ typedef enum { PPX_UPDATE_NONE = 0, PPX_UPDATE_SGD = 1, PPX_UPDATE_ADAM = 2 } pp
 typedef struct {
   int32_t s, k, p, rank;
   const void* w;        /* flat parameter block in the call's dtype (what the GEMMs read) */
-  const float* master;  /* flat fp32 block; the bias is read from here (may equal w for FP32) */
+  const float* master;  /* flat fp32 block (may equal w for FP32) */
+  const float* bias;    /* [s] fp32 bias; NULL = the bias slot of `master` */
 } ppx_layer;
+
+/* parts of a layer's gradient (ppx_param_grads / ppx_wgrad) */
+enum { PPX_GRAD_LOCAL = 1, PPX_GRAD_COMP = 2, PPX_GRAD_DEC = 4, PPX_GRAD_BIAS = 8, PPX_GRAD_ALL = 15 };
 
 /* Optimizer fused into the weight-gradient epilogue (training.py:74-105). */
 typedef struct {
@@ -101,6 +105,8 @@ ppx_status ppx_create(int32_t world, int32_t rank, int32_t device, const uint8_t
 ppx_status ppx_destroy(ppx_ctx* ctx);
 const char* ppx_last_error(const ppx_ctx* ctx);
 int32_t ppx_num_sms(const ppx_ctx* ctx);
+/* Pre-allocate the FP32-tier split workspace (needed before CUDA-graph capture of FP32 calls). */
+ppx_status ppx_reserve_workspace(ppx_ctx* ctx, int64_t bytes);
 
 /* ---- phantom-parallel layer ops -------------------------------------------------------- */
 
@@ -157,12 +163,31 @@ ppx_status ppx_all_reduce(ppx_ctx* ctx, ppx_dtype dt, void* buf, int64_t count, 
 /* phantom.py:239-267 — parameter gradients of one layer (fp32, flat layout `grad`):
      local = delta^T y_prev, compressor = r^T y_prev, decompressor_i = delta^T g_i,
      bias = sum_batch delta.   received r is [B, ldk] (slot `rank` of the reduced buffer).
-   With upd != NULL and upd->kind != NONE the optimizer is applied in the same epilogue
-   (bias excluded: see ppx_bias_update); grad may then be NULL. */
+   `parts` (PPX_GRAD_*) selects which gradients are formed.  With upd != NULL and upd->kind !=
+   NONE the optimizer is applied in the same epilogue (the bias part is never fused: use
+   ppx_optimizer_step on the bias gradient); grad may then be NULL. */
 ppx_status ppx_param_grads(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B,
                            const void* delta, int64_t ld_d, const void* y_prev, int64_t ld_y,
                            const void* phantoms, const void* received, float* grad,
-                           const ppx_update* upd, int32_t with_bias, void* stream);
+                           const ppx_update* upd, int32_t parts, void* stream);
+
+/* Several layers' / ranks' weight gradients in ONE grouped tcgen05 launch (up to 8 problems):
+   the engine overlaps the reduce-scatter of layer l with {d local_l, d decompressor_l,
+   d compressor_{l+1}} this way. */
+typedef struct {
+  const ppx_layer* layer;
+  int32_t parts;
+  int32_t B;
+  const void* delta;
+  int64_t ld_d;
+  const void* y_prev;
+  int64_t ld_y;
+  const void* phantoms;
+  const void* received;
+  float* grad;
+  const ppx_update* upd;
+} ppx_wgrad_item;
+ppx_status ppx_wgrad(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad_item* items, void* stream);
 
 /* phantom.py:210-236 — delta_prev = (local^T delta + compressor^T r) * act'(pre_prev): ONE
    K-concatenated contraction [delta | r] . [L ; C]; `mask_src` is pre_prev or y_prev (only its
@@ -190,6 +215,7 @@ ppx_status ppx_gemm(ppx_ctx* ctx, ppx_dtype dt, int32_t M, int32_t N, int32_t K,
                     const ppx_epilogue* epi, void* stream);
 
 /* elementwise helpers used by the host engine */
+ppx_status ppx_zero(ppx_ctx* ctx, void* ptr, int64_t bytes, void* stream); /* cudaMemsetAsync */
 ppx_status ppx_cast(ppx_ctx* ctx, ppx_dtype src_dt, const void* src, ppx_dtype dst_dt, void* dst,
                     int64_t n, void* stream);
 /* y = act(x + bias) over [rows, cols] (TP row-parallel epilogue after the all-reduce);

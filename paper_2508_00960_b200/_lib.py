@@ -30,13 +30,24 @@ _fp = ctypes.c_void_p  # float*
 
 class Layer(ctypes.Structure):
     """ppx_layer: one logical rank's shard of one layer."""
-    _fields_ = [("s", _i32), ("k", _i32), ("p", _i32), ("rank", _i32), ("w", _vp), ("master", _vp)]
+    _fields_ = [("s", _i32), ("k", _i32), ("p", _i32), ("rank", _i32), ("w", _vp), ("master", _vp),
+                ("bias", _vp)]
 
 
 class Update(ctypes.Structure):
     """ppx_update: optimizer fused into the weight-gradient epilogue."""
     _fields_ = [("kind", _i32), ("hyper", _vp), ("master", _vp), ("w_next", _vp),
                 ("adam_m", _vp), ("adam_v", _vp), ("grad", _vp), ("bad", _vp)]
+
+
+class WgradItem(ctypes.Structure):
+    """ppx_wgrad_item: one layer's weight-gradient request in a grouped launch."""
+    _fields_ = [("layer", ctypes.POINTER(Layer)), ("parts", _i32), ("B", _i32), ("delta", _vp), ("ld_d", _i64),
+                ("y_prev", _vp), ("ld_y", _i64), ("phantoms", _vp), ("received", _vp), ("grad", _vp),
+                ("upd", ctypes.POINTER(Update))]
+
+
+GRAD_LOCAL, GRAD_COMP, GRAD_DEC, GRAD_BIAS, GRAD_ALL = 1, 2, 4, 8, 15
 
 
 class Epilogue(ctypes.Structure):
@@ -53,6 +64,7 @@ _SIGS = {
     "ppx_destroy": (_i32, [_vp]),
     "ppx_last_error": (ctypes.c_char_p, [_vp]),
     "ppx_num_sms": (_i32, [_vp]),
+    "ppx_reserve_workspace": (_i32, [_vp, _i64]),
     "ppx_compress": (_i32, [_vp, _i32, ctypes.POINTER(Layer), _i32, _vp, _i64, _vp, _vp]),
     "ppx_all_gather": (_i32, [_vp, _i32, _vp, _i64, _i32, _vp]),
     "ppx_forward_update": (_i32, [_vp, _i32, ctypes.POINTER(Layer), _i32, _i32, _vp, _i64, _vp,
@@ -67,12 +79,14 @@ _SIGS = {
     "ppx_all_reduce": (_i32, [_vp, _i32, _vp, _i64, _vp]),
     "ppx_param_grads": (_i32, [_vp, _i32, ctypes.POINTER(Layer), _i32, _vp, _i64, _vp, _i64, _vp,
                                _vp, _fp, ctypes.POINTER(Update), _i32, _vp]),
+    "ppx_wgrad": (_i32, [_vp, _i32, _i32, ctypes.POINTER(WgradItem), _vp]),
     "ppx_backward_delta": (_i32, [_vp, _i32, ctypes.POINTER(Layer), _i32, _i32, _vp, _i64, _vp,
                                   _vp, _i64, _vp, _i64, _fp, _vp]),
     "ppx_colsum": (_i32, [_vp, _i32, _i32, _i32, _vp, _i64, _fp, _i32, _vp]),
     "ppx_optimizer_step": (_i32, [_vp, _i32, _fp, _fp, _fp, _fp, _fp, _i64, _i32, _vp, _vp, _vp]),
     "ppx_gemm": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _i64, _i32, _vp, _i64,
                         _i32, ctypes.POINTER(Epilogue), _vp]),
+    "ppx_zero": (_i32, [_vp, _vp, _i64, _vp]),
     "ppx_cast": (_i32, [_vp, _i32, _vp, _i32, _vp, _i64, _vp]),
     "ppx_bias_act": (_i32, [_vp, _i32, _i32, _i32, _vp, _i64, _fp, _i32, _vp, _i64, _vp]),
     "ppx_relu_mask": (_i32, [_vp, _i32, _i32, _i32, _vp, _i64, _vp, _i64, _vp]),

@@ -38,8 +38,8 @@ constexpr int A_STAGE_BYTES = BM * ROW_BYTES;          // 16 KB
 constexpr int B_STAGE_BYTES = BN_MAX * ROW_BYTES;      // 32 KB
 constexpr int NUM_THREADS = 256;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 spare, w4-7 epilogue
 constexpr int TMEM_COLS = 512;    // 2 accumulator stages x 256 fp32 columns
-constexpr int MAX_MAPS = 16;
-constexpr int MAX_PROBS = 4;
+constexpr int MAX_MAPS = 24;
+constexpr int MAX_PROBS = 8;
 constexpr int MAX_SEGS = 6;
 constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
 

@@ -393,6 +393,18 @@ ppx_status ppx_destroy(ppx_ctx* ctx) {
 const char* ppx_last_error(const ppx_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 int32_t ppx_num_sms(const ppx_ctx* ctx) { return ctx ? ctx->num_sms : 0; }
 
+ppx_status ppx_reserve_workspace(ppx_ctx* ctx, int64_t bytes) {
+  if (!ctx || bytes < 0) return PPX_E_CONFIG;
+  if (!ctx->ws.empty() && (int64_t)ctx->ws.front().second >= bytes) return PPX_OK;
+  for (auto& c : ctx->ws) cudaFree(c.first);
+  ctx->ws.clear();
+  if (bytes == 0) return PPX_OK;
+  char* p = nullptr;
+  CUDA_TRY(ctx, cudaMalloc(&p, (size_t)bytes));
+  ctx->ws.push_back({p, (size_t)bytes});
+  return PPX_OK;
+}
+
 // ---------------------------------------------------------------------------------------------
 ppx_status ppx_compress(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, const void* y_prev, int64_t ld_y,
                         void* phantoms, void* stream) {
@@ -427,7 +439,7 @@ static ppx_status forward_common(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L,
     b.add_segment(pr, g, d, kpb * (L->p - 1), kpb);
   }
   if (pr) {
-    pr->epi.bias = L->master + f.bias;
+    pr->epi.bias = L->bias ? L->bias : L->master + f.bias;
     pr->epi.flags = ppx::EP_BIAS | (act == PPX_RELU ? ppx::EP_RELU : 0u);
   }
   return b.ok() ? PPX_OK : b.status;
@@ -564,27 +576,27 @@ static void set_update(ppx::Epilogue& E, const ppx_update* upd, ppx_dtype dt, in
   E.bad = upd->bad;
 }
 
-ppx_status ppx_param_grads(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, const void* delta,
-                           int64_t ld_d, const void* y_prev, int64_t ld_y, const void* phantoms,
-                           const void* received, float* grad, const ppx_update* upd, int32_t with_bias,
-                           void* stream) {
-  if (!ctx) return PPX_E_CONFIG;
+static ppx_status wgrad_add(ppx_ctx* ctx, ppx_dtype dt, Builder& b, const ppx_wgrad_item& it) {
+  const ppx_layer* L = it.layer;
+  const ppx_update* upd = it.upd;
+  const int32_t B = it.B;
   const bool update = upd && upd->kind != PPX_UPDATE_NONE;
-  if (bad_layer(L) || B < 1 || !delta || !y_prev || (!grad && !update))
-    return fail(ctx, PPX_E_CONFIG, "ppx_param_grads: bad arguments");
+  float* grad = it.grad;
+  if (bad_layer(L) || B < 1 || !it.delta || !it.y_prev || (!grad && !update))
+    return fail(ctx, PPX_E_CONFIG, "param grads: bad arguments");
   if (update && (!upd->master || !upd->hyper || (upd->kind == PPX_UPDATE_ADAM && (!upd->adam_m || !upd->adam_v))))
-    return fail(ctx, PPX_E_CONFIG, "ppx_param_grads: incomplete update");
-  if (L->p > 1 && (!phantoms || !received))
-    return fail(ctx, PPX_E_SEQUENCING, "ppx_param_grads: phantom tape or received gradient missing");
+    return fail(ctx, PPX_E_CONFIG, "param grads: incomplete update");
+  const bool need_r = L->p > 1 && (it.parts & PPX_GRAD_COMP);
+  const bool need_g = L->p > 1 && (it.parts & PPX_GRAD_DEC);
+  if ((need_r && !it.received) || (need_g && !it.phantoms))
+    return fail(ctx, PPX_E_SEQUENCING, "param grads: phantom tape or received gradient missing");
   Flat f(L->s, L->k, L->p);
-  Builder b(ctx, dt, stream);
   const int kt = (int)cdiv(B, b.BK);
-  // d local = delta^T y_prev   [s, s]
-  {
+  if (it.parts & PPX_GRAD_LOCAL) {  // d local = delta^T y_prev   [s, s]
     Problem* pr = b.new_problem(L->s, L->s, 1, true);
-    Opnd a{view2(delta, B, L->s, ld_d)};
+    Opnd a{view2(it.delta, B, L->s, it.ld_d)};
     a.mn = 1;
-    Opnd y{view2(y_prev, B, L->s, ld_y)};
+    Opnd y{view2(it.y_prev, B, L->s, it.ld_y)};
     y.mn = 1;
     b.add_segment(pr, a, y, kt, kt);
     if (pr) {
@@ -592,23 +604,25 @@ ppx_status ppx_param_grads(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32
       else pr->epi.out = t2(grad + f.local, f.lds, 1);
     }
   }
-  // d compressor = r^T y_prev   [k, s]   (r is zero when p == 1: skip, gradient is zero)
-  if (L->p > 1) {
+  if (need_r) {  // d compressor = r^T y_prev   [k, s]
     Problem* pr = b.new_problem(L->k, L->s, 1, true);
-    Opnd r{view2(received, B, L->k, f.ldk)};
+    Opnd r{view2(it.received, B, L->k, f.ldk)};
     r.mn = 1;
-    Opnd y{view2(y_prev, B, L->s, ld_y)};
+    Opnd y{view2(it.y_prev, B, L->s, it.ld_y)};
     y.mn = 1;
     b.add_segment(pr, r, y, kt, kt);
     if (pr) {
       if (update) set_update(pr->epi, upd, dt, f.comp, f.lds, 0);
       else pr->epi.out = t2(grad + f.comp, f.lds, 1);
     }
-    // d decompressor_q = delta^T g_{src(q)}   [p-1][s, k]
+  } else if ((it.parts & PPX_GRAD_COMP) && grad) {  // p == 1: no peers, zero gradient
+    cudaMemsetAsync(grad + f.comp, 0, sizeof(float) * L->k * f.lds, b.st);
+  }
+  if (need_g) {  // d decompressor_q = delta^T g_{src(q)}   [p-1][s, k]
     Problem* pd = b.new_problem(L->s, L->k, L->p - 1, true);
-    Opnd a{view2(delta, B, L->s, ld_d)};
+    Opnd a{view2(it.delta, B, L->s, it.ld_d)};
     a.mn = 1;
-    Opnd g{view3(phantoms, L->p, B, L->k, f.ldk, (int64_t)B * f.ldk)};
+    Opnd g{view3(it.phantoms, L->p, B, L->k, f.ldk, (int64_t)B * f.ldk)};
     g.mn = 1;
     g.slot_src = 2;
     g.slot_skip = L->rank;
@@ -617,14 +631,39 @@ ppx_status ppx_param_grads(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32
       if (update) set_update(pd->epi, upd, dt, f.dec, f.ldk, (int64_t)L->s * f.ldk);
       else pd->epi.out = t2(grad + f.dec, f.ldk, 1, (int64_t)L->s * f.ldk);
     }
-  } else if (grad) {
-    cudaMemsetAsync(grad + f.comp, 0, sizeof(float) * L->k * f.lds, (cudaStream_t)stream);
+  }
+  return b.ok() ? PPX_OK : b.status;
+}
+
+static ppx_status wgrad_bias(ppx_ctx* ctx, ppx_dtype dt, const ppx_wgrad_item& it, cudaStream_t st) {
+  if (!(it.parts & PPX_GRAD_BIAS) || !it.grad) return PPX_OK;
+  Flat f(it.layer->s, it.layer->k, it.layer->p);
+  cudaError_t e = ppx::launch_colsum(dt == PPX_FP32, it.B, it.layer->s, it.delta, it.ld_d, it.grad + f.bias, 0, st);
+  return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "colsum: %s", cudaGetErrorString(e));
+}
+
+ppx_status ppx_param_grads(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, const void* delta,
+                           int64_t ld_d, const void* y_prev, int64_t ld_y, const void* phantoms,
+                           const void* received, float* grad, const ppx_update* upd, int32_t parts,
+                           void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  ppx_wgrad_item it{L, parts, B, delta, ld_d, y_prev, ld_y, phantoms, received, grad, upd};
+  return ppx_wgrad(ctx, dt, 1, &it, stream);
+}
+
+ppx_status ppx_wgrad(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad_item* items, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (nitems < 0 || (nitems > 0 && !items)) return fail(ctx, PPX_E_CONFIG, "ppx_wgrad: bad arguments");
+  Builder b(ctx, dt, stream);
+  for (int i = 0; i < nitems; ++i) {
+    ppx_status s = wgrad_add(ctx, dt, b, items[i]);
+    if (s != PPX_OK) return s;
   }
   ppx_status s = b.launch();
   if (s != PPX_OK) return s;
-  if (with_bias && grad) {
-    cudaError_t e = ppx::launch_colsum(dt == PPX_FP32, B, L->s, delta, ld_d, grad + f.bias, 0, (cudaStream_t)stream);
-    if (e != cudaSuccess) return fail(ctx, PPX_E_CUDA, "colsum: %s", cudaGetErrorString(e));
+  for (int i = 0; i < nitems; ++i) {
+    s = wgrad_bias(ctx, dt, items[i], (cudaStream_t)stream);
+    if (s != PPX_OK) return s;
   }
   return PPX_OK;
 }
@@ -712,6 +751,14 @@ ppx_status ppx_gemm(ppx_ctx* ctx, ppx_dtype dt, int32_t M, int32_t N, int32_t K,
     }
   }
   return b.launch();
+}
+
+ppx_status ppx_zero(ppx_ctx* ctx, void* ptr, int64_t bytes, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (bytes < 0 || (bytes > 0 && !ptr)) return fail(ctx, PPX_E_CONFIG, "ppx_zero: bad arguments");
+  if (bytes == 0) return PPX_OK;
+  CUDA_TRY(ctx, cudaMemsetAsync(ptr, 0, (size_t)bytes, (cudaStream_t)stream));
+  return PPX_OK;
 }
 
 ppx_status ppx_cast(ppx_ctx* ctx, ppx_dtype src_dt, const void* src, ppx_dtype dst_dt, void* dst, int64_t n,

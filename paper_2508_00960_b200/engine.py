@@ -1,0 +1,348 @@
+"""PhantomEngine — the throughput path: one process per GPU, NCCL over NVLink, CUDA graphs.
+
+The engine runs `pp_iteration` + the optimizer (reference training.py:181-213, 276-309) for the
+logical ranks this GPU owns, natively in [batch, features] layout, with every dense contraction
+in the tcgen05 kernel and these fusions:
+
+  forward  layer l:  compress (K2) -> phantom all-gather on the comm stream -> ONE
+                     K-concatenated local+decompress GEMM with bias+ReLU epilogue (K1); the
+                     output layer's epilogue also forms delta_L, the loss partial and d bias (K7/K8).
+  backward layer l:  error compression D^T delta (K3) -> reduce-scatter on the comm stream,
+                     overlapped with the grouped weight-gradient launch {d local_l, d decomp_l,
+                     d compressor_{l+1}} whose epilogue applies SGD/Adam in place (K4/K5/K9);
+                     then [delta | r].[L ; C] with the ReLU'-mask + d bias epilogue (K6/K8).
+
+Logical rank j lives on GPU j // R (R = p / world).  Weights are fp32 masters plus two bf16
+compute copies (read one, write the other: the update of step t never races the GEMMs of step
+t that still read the old weights).  Each step is captured once per parity in a CUDA graph.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+
+from . import _lib, kernels
+from .core import Activation, as_activation, flat_offsets, round8
+from .errors import ConfigurationError, TrainingError
+
+
+def pp_step_flops(n: int, p: int, k: int, layers: int, batch: int) -> int:
+    """Algorithmic GEMM FLOPs of one training step for ONE logical rank:
+    6 L B s (s + p k) - 2 B s (s + k)  (layer 0 has no error recurrence)."""
+    s = n // p
+    return 6 * layers * batch * s * (s + p * k) - 2 * batch * s * (s + k)
+
+
+def pp_forward_flops(n: int, p: int, k: int, layers: int, batch: int) -> int:
+    s = n // p
+    return 2 * layers * batch * s * (s + p * k)
+
+
+class PhantomEngine:
+    def __init__(self, n: int, p: int, k: int, layers: int, batch: int, *, world: int = 1, rank: int = 0,
+                 device: int = 0, uid: bytes | None = None, activation=Activation.RELU, reduction: str = "mean",
+                 optimizer: str = "sgd", lr: float = 1e-4, betas=(0.9, 0.999), eps: float = 1e-8,
+                 dtype: torch.dtype = torch.bfloat16, seed: int = 0, ctx: _lib.Context | None = None):
+        if n % p:
+            raise ConfigurationError(f"n={n} not divisible by p={p}")
+        if p % world:
+            raise ConfigurationError(f"p={p} logical ranks do not divide over {world} GPUs")
+        s = n // p
+        if not 1 <= k <= s:
+            raise ConfigurationError(f"need 1 <= k <= n/p, got k={k}, n/p={s}")
+        if optimizer not in ("sgd", "adam"):
+            raise ConfigurationError("optimizer must be sgd or adam")
+        self.n, self.p, self.k, self.L, self.B, self.s = n, p, k, layers, batch, s
+        self.world, self.rank, self.R = world, rank, p // world
+        self.local = list(range(rank * self.R, (rank + 1) * self.R))
+        self.act = as_activation(activation)
+        self.reduction, self.optimizer, self.lr, self.betas, self.eps = reduction, optimizer, lr, betas, eps
+        self.dtype = dtype
+        self.pdt = kernels.ppx_dtype(dtype)
+        self.dev = torch.device("cuda", device)
+        torch.cuda.set_device(self.dev)
+        self.ctx = ctx or _lib.Context(world, rank, device, uid)
+        self.comm_stream = torch.cuda.Stream(self.dev)
+        self.copy_stream = torch.cuda.Stream(self.dev)
+        self.off = flat_offsets(s, k, p)
+        T, R, L, B = self.off["total"], self.R, layers, batch
+        ldk = self.off["ldk"]
+        f32 = torch.float32
+        # parameters
+        self.master = torch.zeros((R, L, T), dtype=f32, device=self.dev)
+        # two compute copies (read w[par], the fused update writes w[1-par]); separate from the
+        # master even in the fp32 tier so an in-place update never races a GEMM of the same step
+        self.w = [torch.zeros((R, L, T), dtype=dtype, device=self.dev) for _ in range(2)]
+        self.bias = torch.zeros((R, L, s), dtype=f32, device=self.dev)
+        self.gbias = torch.zeros((R, L, s), dtype=f32, device=self.dev)
+        if optimizer == "adam":
+            self.adam_m = torch.zeros_like(self.master)
+            self.adam_v = torch.zeros_like(self.master)
+            self.adam_bm = torch.zeros_like(self.bias)
+            self.adam_bv = torch.zeros_like(self.bias)
+        self.t = 0
+        self._init_weights(seed)
+        # activations: Y[parity][jj][l], l = 0 (input) .. L (output); targets per parity
+        self.Y = [[[torch.empty((B, s), dtype=dtype, device=self.dev) for _ in range(L + 1)] for _ in range(R)]
+                  for _ in range(2)]
+        # the inner layers' activations are shared between parities (only inputs double-buffer)
+        for jj in range(R):
+            for l in range(1, L + 1):
+                self.Y[1][jj][l] = self.Y[0][jj][l]
+        self.Tgt = [[torch.empty((B, s), dtype=dtype, device=self.dev) for _ in range(R)] for _ in range(2)]
+        self.D = [[torch.empty((B, s), dtype=dtype, device=self.dev) for _ in range(2)] for _ in range(R)]
+        self.G = [torch.zeros((p, B, ldk), dtype=dtype, device=self.dev) for _ in range(L)]
+        self.H = [torch.zeros((p, B, ldk), dtype=dtype, device=self.dev) for _ in range(L)]
+        self.loss = torch.zeros(1, dtype=f32, device=self.dev)
+        self.bad = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.hyper = torch.zeros(6, dtype=f32, device=self.dev)
+        self.hyper_host = torch.zeros(6, dtype=f32).pin_memory()
+        self.out_host = torch.zeros(1, dtype=f32).pin_memory()
+        self.bad_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+        if dtype == torch.float32:   # 3xTF32 hi/lo splits: reserve so graph capture never allocates
+            per_call = 4 * B * s + 2 * p * B * ldk + 2 * T + 4 * s * ldk
+            self.ctx.call("ppx_reserve_workspace", int(2 * 4 * per_call * 1.25) + (1 << 20))
+        self.graphs = [None, None]
+        self.parity = 0
+        self._keep = []   # ctypes structs referenced by captured launches
+
+    # ------------------------------------------------------------------------------------------
+    def _init_weights(self, seed):
+        """Glorot-uniform bounds of the reference init (phantom.py:126-129), drawn on device."""
+        s, k, p, off = self.s, self.k, self.p, self.off
+        g = torch.Generator(device=self.dev)
+        lds, ldk = off["lds"], off["ldk"]
+        for jj, j in enumerate(self.local):
+            for l in range(self.L):
+                g.manual_seed((seed * 1_000_003 + l * 1009 + j) & 0x7FFFFFFF)
+                m = self.master[jj, l]
+                a = math.sqrt(6.0 / (2 * s))
+                m[0:s * lds].view(s, lds)[:, :s].uniform_(-a, a, generator=g)
+                a = math.sqrt(6.0 / (s + k))
+                m[off["comp"]:off["comp"] + k * lds].view(k, lds)[:, :s].uniform_(-a, a, generator=g)
+                if p > 1:
+                    m[off["dec"]:off["bias"]].view(p - 1, s, ldk)[:, :, :k].uniform_(-a, a, generator=g)
+        self.refresh_compute_copy()
+
+    def refresh_compute_copy(self):
+        st = torch.cuda.current_stream().cuda_stream
+        for w in self.w:
+            self.ctx.call("ppx_cast", _lib.PPX_FP32, self.master.data_ptr(), self.pdt, w.data_ptr(),
+                          self.master.numel(), st)
+
+    def load_params(self, rank_layers):
+        """Copy reference-format shards (dicts / PhantomLayers, numpy or torch) of this GPU's
+        logical ranks into the engine (weights identical to the oracle for parity runs)."""
+        s, k, p, off = self.s, self.k, self.p, self.off
+        lds, ldk = off["lds"], off["ldk"]
+        for jj, j in enumerate(self.local):
+            for l in range(self.L):
+                lay = rank_layers[j][l]
+                get = (lambda nm: lay[nm]) if isinstance(lay, dict) else (lambda nm: getattr(lay, nm))
+                m = self.master[jj, l]
+                m[0:s * lds].view(s, lds)[:, :s].copy_(torch.as_tensor(get("local"), dtype=torch.float64))
+                m[off["comp"]:off["comp"] + k * lds].view(k, lds)[:, :s].copy_(
+                    torch.as_tensor(get("compressor"), dtype=torch.float64))
+                decs = get("decompressors")
+                for q in range(p - 1):
+                    i = q + (1 if q >= j else 0)
+                    base = off["dec"] + q * s * ldk
+                    m[base:base + s * ldk].view(s, ldk)[:, :k].copy_(torch.as_tensor(decs[i], dtype=torch.float64))
+                self.bias[jj, l].copy_(torch.as_tensor(get("bias"), dtype=torch.float64))
+        self.refresh_compute_copy()
+
+    def layer_views(self, jj, l):
+        """Reference-shaped views (local, compressor, {src: decompressor}, bias) of one shard."""
+        s, k, p, off = self.s, self.k, self.p, self.off
+        lds, ldk = off["lds"], off["ldk"]
+        m = self.master[jj, l]
+        j = self.local[jj]
+        decs = {}
+        for q in range(p - 1):
+            i = q + (1 if q >= j else 0)
+            base = off["dec"] + q * s * ldk
+            decs[i] = m[base:base + s * ldk].view(s, ldk)[:, :k]
+        return {"local": m[0:s * lds].view(s, lds)[:, :s], "compressor": m[off["comp"]:off["comp"] + k * lds]
+                .view(k, lds)[:, :s], "decompressors": decs, "bias": self.bias[jj, l]}
+
+    # ------------------------------------------------------------------------------------------
+    def _layer(self, jj, l, par):
+        L = _lib.Layer(self.s, self.k, self.p, self.local[jj], self.w[par][jj, l].data_ptr(),
+                       self.master[jj, l].data_ptr(), self.bias[jj, l].data_ptr())
+        self._keep.append(L)
+        return L
+
+    def _update(self, jj, l, par):
+        kind = _lib.PPX_UPDATE_ADAM if self.optimizer == "adam" else _lib.PPX_UPDATE_SGD
+        u = _lib.Update(kind, self.hyper.data_ptr(), self.master[jj, l].data_ptr(),
+                        self.w[1 - par][jj, l].data_ptr(),
+                        self.adam_m[jj, l].data_ptr() if kind == _lib.PPX_UPDATE_ADAM else None,
+                        self.adam_v[jj, l].data_ptr() if kind == _lib.PPX_UPDATE_ADAM else None,
+                        None, self.bad.data_ptr())
+        self._keep.append(u)
+        return u
+
+    def _received(self, l, j):
+        return self.H[l].data_ptr() + j * self.B * self.off["ldk"] * self.H[l].element_size()
+
+    @staticmethod
+    def _join(src: torch.cuda.Stream, dst: torch.cuda.Stream):
+        ev = torch.cuda.Event()
+        ev.record(src)
+        dst.wait_event(ev)
+
+    def _forward(self, par, S, train=True):
+        c, st, pdt, B, s = self.ctx, S.cuda_stream, self.pdt, self.B, self.s
+        slot = B * self.off["ldk"]
+        for l in range(self.L):
+            for jj in range(self.R):
+                y = self.Y[par][jj][l]
+                c.call("ppx_compress", pdt, ctypes.byref(self._layer(jj, l, par)), B, y.data_ptr(), s,
+                       self.G[l].data_ptr(), st)
+            if self.world > 1:
+                self._join(S, self.comm_stream)
+                c.call("ppx_all_gather", pdt, self.G[l].data_ptr(), slot, self.R, self.comm_stream.cuda_stream)
+                self._join(self.comm_stream, S)
+            for jj in range(self.R):
+                y = self.Y[par][jj][l]
+                out = self.Y[par][jj][l + 1]
+                lay = ctypes.byref(self._layer(jj, l, par))
+                if l < self.L - 1 or not train:
+                    c.call("ppx_forward_update", pdt, lay, B, self.act.code, y.data_ptr(), s, self.G[l].data_ptr(),
+                           out.data_ptr(), s, None, 0, st)
+                else:
+                    mean = self.reduction == "mean"
+                    c.call("ppx_forward_output", pdt, lay, B, self.act.code, y.data_ptr(), s, self.G[l].data_ptr(),
+                           out.data_ptr(), s, self.Tgt[par][jj].data_ptr(), s, self.D[jj][0].data_ptr(), s,
+                           1.0 / B if mean else 1.0, 0.5 / B if mean else 0.5, self.loss.data_ptr(),
+                           self.gbias[jj, l].data_ptr(), st)
+
+    def _backward(self, par, S):
+        c, st, pdt, B, s, R, L = self.ctx, S.cuda_stream, self.pdt, self.B, self.s, self.R, self.L
+        slot = B * self.off["ldk"]
+        esz = self.H[0].element_size()
+        cur = 0
+        for l in range(L - 1, -1, -1):
+            if R > 1:  # several local ranks accumulate into the same contribution slots
+                c.call("ppx_zero", self.H[l].data_ptr(), self.H[l].numel() * esz, st)
+            for jj in range(R):
+                c.call("ppx_error_phantoms", pdt, ctypes.byref(self._layer(jj, l, par)), B,
+                       self.D[jj][cur].data_ptr(), s, self.H[l].data_ptr(), int(R > 1), st)
+            if self.world > 1:
+                self._join(S, self.comm_stream)
+                c.call("ppx_reduce_scatter", pdt, self.H[l].data_ptr(), slot, R, self.comm_stream.cuda_stream)
+            # weight gradients that do not need r_l, overlapped with the reduce-scatter
+            for jj in range(R):
+                j = self.local[jj]
+                items = [_lib.WgradItem(ctypes.pointer(self._layer(jj, l, par)), _lib.GRAD_LOCAL | _lib.GRAD_DEC, B,
+                                        self.D[jj][cur].data_ptr(), s, self.Y[par][jj][l].data_ptr(), s,
+                                        self.G[l].data_ptr(), None, None, ctypes.pointer(self._update(jj, l, par)))]
+                if l < L - 1:   # d compressor of layer l+1 (its r arrived one layer ago)
+                    items.append(_lib.WgradItem(ctypes.pointer(self._layer(jj, l + 1, par)), _lib.GRAD_COMP, B,
+                                                self.D[jj][cur].data_ptr(), s, self.Y[par][jj][l + 1].data_ptr(), s,
+                                                None, self._received(l + 1, j), None,
+                                                ctypes.pointer(self._update(jj, l + 1, par))))
+                arr = (_lib.WgradItem * len(items))(*items)
+                self._keep.append(arr)
+                c.call("ppx_wgrad", pdt, len(items), arr, st)
+            if self.world > 1:
+                self._join(self.comm_stream, S)
+            if l > 0:
+                for jj in range(R):
+                    j = self.local[jj]
+                    y_prev = self.Y[par][jj][l]
+                    c.call("ppx_backward_delta", pdt, ctypes.byref(self._layer(jj, l, par)), B, self.act.code,
+                           self.D[jj][cur].data_ptr(), s, self._received(l, j),
+                           y_prev.data_ptr() if self.act is Activation.RELU else None, s,
+                           self.D[jj][1 - cur].data_ptr(), s, self.gbias[jj, l - 1].data_ptr(), st)
+                cur = 1 - cur
+        for jj in range(R):   # d compressor of layer 0
+            j = self.local[jj]
+            items = [_lib.WgradItem(ctypes.pointer(self._layer(jj, 0, par)), _lib.GRAD_COMP, B,
+                                    self.D[jj][cur].data_ptr(), s, self.Y[par][jj][0].data_ptr(), s, None,
+                                    self._received(0, j), None, ctypes.pointer(self._update(jj, 0, par)))]
+            arr = (_lib.WgradItem * 1)(*items)
+            self._keep.append(arr)
+            c.call("ppx_wgrad", pdt, 1, arr, st)
+        # biases of all local ranks and layers in one elementwise launch
+        kind = _lib.PPX_UPDATE_ADAM if self.optimizer == "adam" else _lib.PPX_UPDATE_SGD
+        c.call("ppx_optimizer_step", kind, self.hyper.data_ptr(), self.bias.data_ptr(), self.gbias.data_ptr(),
+               self.adam_bm.data_ptr() if kind == _lib.PPX_UPDATE_ADAM else None,
+               self.adam_bv.data_ptr() if kind == _lib.PPX_UPDATE_ADAM else None,
+               self.bias.numel(), _lib.PPX_FP32, None, self.bad.data_ptr(), st)
+
+    def _step_body(self, par, S):
+        self._keep.clear()
+        c, st = self.ctx, S.cuda_stream
+        c.call("ppx_zero", self.gbias.data_ptr(), self.gbias.numel() * 4, st)
+        c.call("ppx_zero", self.loss.data_ptr(), 4, st)
+        self._forward(par, S)
+        self._backward(par, S)
+        if self.world > 1:
+            c.call("ppx_all_reduce_f32", self.loss.data_ptr(), 1, st)
+
+    # ------------------------------------------------------------------------------------------
+    def _set_hyper(self):
+        self.t += 1
+        b1, b2 = self.betas
+        self.hyper_host.copy_(torch.tensor([self.lr, b1, b2, self.eps, 1 - b1 ** self.t, 1 - b2 ** self.t]))
+
+    def step(self, graph: bool = True):
+        """One training iteration on the device-resident batch of the current parity."""
+        par = self.parity
+        S = torch.cuda.current_stream()
+        self._set_hyper()
+        self.hyper.copy_(self.hyper_host, non_blocking=True)
+        if graph and self.graphs[par] is not None:
+            self.graphs[par].replay()
+        else:
+            self._step_body(par, S)
+        self.parity = 1 - par
+
+    def capture(self):
+        """Capture one CUDA graph per parity (weights / input double buffers alternate)."""
+        torch.cuda.synchronize()
+        for par in (0, 1):
+            g = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream(self.dev)
+            cs.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.graph(g, stream=cs):
+                self._step_body(par, torch.cuda.current_stream())
+            self.graphs[par] = g
+        torch.cuda.synchronize()
+
+    def forward_only(self, par=None):
+        """Inference (config C5): the forward loop without tape, loss or delta."""
+        par = self.parity if par is None else par
+        self._forward(par, torch.cuda.current_stream(), train=False)
+        return [self.Y[par][jj][self.L] for jj in range(self.R)]
+
+    # ------------------------------------------------------------------------------------------
+    def set_batch(self, x_shards, t_shards, par=None):
+        """Device tensors (B, s) per local rank -> input/target buffers of a parity."""
+        par = self.parity if par is None else par
+        for jj in range(self.R):
+            self.Y[par][jj][0].copy_(x_shards[jj])
+            self.Tgt[par][jj].copy_(t_shards[jj])
+
+    def load_batch_async(self, x_host, t_host, par):
+        """H2D of one step's inputs (pinned host [R, B, s] each) on the copy stream; returns the
+        event the compute stream must wait on."""
+        with torch.cuda.stream(self.copy_stream):
+            for jj in range(self.R):
+                self.Y[par][jj][0].copy_(x_host[jj], non_blocking=True)
+                self.Tgt[par][jj].copy_(t_host[jj], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.copy_stream)
+        return ev
+
+    def read_loss(self) -> float:
+        self.out_host.copy_(self.loss, non_blocking=True)
+        self.bad_host.copy_(self.bad, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        if int(self.bad_host[0]) != 0:
+            raise TrainingError("non-finite gradient detected on the device")
+        return float(self.out_host[0].item())

@@ -113,7 +113,7 @@ class PhantomLayer:
                  self.w.data_ptr(), self.master.numel(), kernels.stream_handle())
 
     def abi(self) -> _lib.Layer:
-        return _lib.Layer(self.s, self.k, self.p, self.rank, self.w.data_ptr(), self.master.data_ptr())
+        return _lib.Layer(self.s, self.k, self.p, self.rank, self.w.data_ptr(), self.master.data_ptr(), None)
 
     @property
     def shard_width(self) -> int:
@@ -439,7 +439,7 @@ def pp_param_grads(layer: PhantomLayer, delta, tape_entry: LayerTape, received_p
     L = layer.abi()
     kernels.ctx_for(d).call("ppx_param_grads", kernels.ppx_dtype(dt), ctypes.byref(L), B, d.data_ptr(),
                             kernels.ld(d), y.data_ptr(), kernels.ld(y), ph.data_ptr(), r.data_ptr(), flat.data_ptr(),
-                            None, 1, kernels.stream_handle())
+                            None, _lib.GRAD_ALL, kernels.stream_handle())
     if counter is not None:
         counter.add(2 * s * s * B + 2 * k * s * B + (p - 1) * 2 * s * k * B + s * B)
     return grads_from_flat(flat, s, k, p, layer.rank)
