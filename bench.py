@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Phantom-parallel FFN training throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config c3]
+
+Workload (config C3, the north_star's headline): width n=16384, 8 layers, p=8 logical phantom
+ranks, k=128, batch 8192, bf16, ReLU, mean half-squared loss, SGD — the SAME model at every N
+(strong scaling): N GPUs each own 8/N logical ranks (N=1 runs all 8 on one GPU, the phantom
+all-gather / reduce-scatter then stay in HBM; N>1 adds NCCL over NVLink).  One step = one
+pp_iteration + optimizer update over one batch of synthetic teacher data (training.py:181-213,
+276-309).  Timed with CUDA events over K CUDA-graph replays, max over ranks.
+
+--impl reference times the reference algorithm's CPU implementation (the numpy oracle port,
+oracle/phantom_oracle.py; the reference itself is pure Python and is not present on the GPU box)
+on this box's host cores on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FFN train samples/s @1/2/4/8 B200, % TC roofline, J/epoch vs tensor-parallel"
+CONFIGS = {
+    "c3": dict(n=16384, p=8, k=128, layers=8, batch=8192),
+    "c2": dict(n=8192, p=4, k=64, layers=8, batch=8192),
+    "c1": dict(n=1024, p=2, k=16, layers=4, batch=64),
+}
+STEPS_PER_EPOCH = 64      # epoch = 64 * B samples
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), d.get("hbm_gbs", 6546.2), "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------------------------
+# clocks / energy
+# ---------------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def energy_mj(gpu_index):
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+        return float(pynvml.nvmlDeviceGetTotalEnergyConsumption(h))
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU baseline / reference arm (oracle port)
+# ---------------------------------------------------------------------------------------------
+def cpu_sample(n, p, k, layers, batch, iters=2):
+    """Time the oracle's pp_iteration (reference algorithm, float64 numpy/OpenBLAS) on the host."""
+    import numpy as np
+    from oracle import phantom_oracle as po
+    s = n // p
+    rng = np.random.default_rng(0)
+    model = []
+    for j in range(p):
+        row = []
+        for _ in range(layers):
+            a = (6.0 / (2 * s)) ** 0.5
+            row.append({"local": rng.uniform(-a, a, (s, s)), "compressor": rng.uniform(-a, a, (k, s)),
+                        "decompressors": {i: rng.uniform(-a, a, (s, k)) for i in range(p) if i != j},
+                        "bias": np.zeros(s)})
+        model.append(row)
+    x = [rng.standard_normal((s, batch)) for _ in range(p)]
+    y = [np.maximum(rng.standard_normal((s, batch)), 0) for _ in range(p)]
+    po.pp_iteration(model, ["relu"] * layers, x, y, "mean")   # warm-up
+    times = []
+    for _ in range(iters):
+        t0 = time.perf_counter()
+        po.pp_iteration(model, ["relu"] * layers, x, y, "mean")
+        times.append(time.perf_counter() - t0)
+    return min(times)
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
+    sample_b = 256
+    n, p, k, L = cfg["n"], cfg["p"], cfg["k"], cfg["layers"]
+    import numpy as np
+    from oracle import phantom_oracle as po
+    s = n // p
+    rng = np.random.default_rng(0)
+    a = (6.0 / (2 * s)) ** 0.5
+    model = [[{"local": rng.uniform(-a, a, (s, s)), "compressor": rng.uniform(-a, a, (k, s)),
+               "decompressors": {i: rng.uniform(-a, a, (s, k)) for i in range(p) if i != j}, "bias": np.zeros(s)}
+              for _ in range(L)] for j in range(p)]
+    x = [rng.standard_normal((s, sample_b)) for _ in range(p)]
+    y = [np.maximum(rng.standard_normal((s, sample_b)), 0) for _ in range(p)]
+    for _ in range(args.warmup):
+        po.pp_iteration(model, ["relu"] * L, x, y, "mean")
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out = po.pp_iteration(model, ["relu"] * L, x, y, "mean")
+        for j in range(p):
+            params, gs = po.pp_param_list(model[j], out["grads"][j])
+            po.sgd_step(params, gs, 1e-4)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = sample_b / dt
+    sample = (f"full {args.config} model (n={n}, p={p}, k={k}, L={L}) float64 pp_iteration+SGD at batch "
+              f"{sample_b} per step (samples/s is linear in batch for this GEMM-bound path)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"phantom FFN {args.config}: n={n}, L={L}, p={p}, k={k}, batch {sample_b} (CPU sample)",
+                   "global_batch": sample_b, "parallelism": f"pp{p} simulated in one process"},
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------------
+def make_data(eng, seed, cfg):
+    """Synthetic teacher data (training.py:43-56 shape): X ~ N(0,1) [B, n]; targets of logical
+    rank j = relu(relu(X) . W_j^T) for a fixed N(0,1)/sqrt(n) teacher, computed on the GPU with
+    the engine's own GEMM (once, outside the timed region)."""
+    import torch
+    from paper_2508_00960_b200 import kernels
+    B, n, s = eng.B, eng.n, eng.s
+    g = torch.Generator(device=eng.dev)
+    g.manual_seed(seed)
+    X = torch.randn((B, n), generator=g, device=eng.dev).to(torch.bfloat16)
+    Xr = torch.empty_like(X)
+    eng.ctx.call("ppx_bias_act", eng.pdt, B, n, X.data_ptr(), n, None, 0, Xr.data_ptr(), n,
+                 torch.cuda.current_stream().cuda_stream)
+    xs, ts = [], []
+    for jj, j in enumerate(eng.local):
+        gt = torch.Generator(device=eng.dev)
+        gt.manual_seed(seed * 7919 + j)
+        W = (torch.randn((s, n), generator=gt, device=eng.dev) / n ** 0.5).to(torch.bfloat16)
+        T = kernels.gemm(Xr, W, transpose_b=True, out_dtype=torch.bfloat16, relu=True, ctx=eng.ctx)
+        xs.append(X[:, j * s:(j + 1) * s].contiguous())
+        ts.append(T)
+        del W
+    del X, Xr
+    return xs, ts
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.batch:
+        cfg["batch"] = args.batch
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2508_00960_b200 import _lib
+    from paper_2508_00960_b200.engine import PhantomEngine, pp_step_flops
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        world = args.gpus if world == 1 and args.gpus == 1 else world
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        uid = [_lib.Context.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        uid = uid[0]
+    else:
+        uid = None
+    n, p, k, L, B = cfg["n"], cfg["p"], cfg["k"], cfg["layers"], cfg["batch"]
+    eng = PhantomEngine(n, p, k, L, B, world=world, rank=rank, device=local_rank, uid=uid,
+                        optimizer="sgd", lr=3e-6, dtype=torch.bfloat16)
+    xs, ts = make_data(eng, 1234, cfg)
+    eng.set_batch(xs, ts, 0)
+    eng.set_batch(xs, ts, 1)
+    use_graph = not args.no_graph
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up: eager step (sets kernel attributes), capture, graph replays
+    eng.step(graph=False)
+    launches_per_step = eng.launch_count
+    if use_graph:
+        eng.capture()
+    for _ in range(max(args.warmup - 1, 2)):
+        eng.step(graph=use_graph)
+    loss0 = eng.read_loss()
+    barrier()
+
+    dev_index = local_rank
+    sampler = ClockSampler(dev_index)
+    sampler.start()
+    e0 = energy_mj(dev_index)
+    S = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev0.record(S)
+    for _ in range(args.steps):
+        eng.step(graph=use_graph)
+    ev1.record(S)
+    barrier()
+    e1 = energy_mj(dev_index)
+    clocks = sampler.stop()
+    t_local = ev0.elapsed_time(ev1) / args.steps   # ms per step
+    loss1 = eng.read_loss()
+
+    t = torch.tensor([t_local], device="cuda")
+    joules = torch.tensor([((e1 - e0) / 1e3 / args.steps) if (e0 is not None and e1 is not None) else float("nan")],
+                          device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(joules, op=dist.ReduceOp.SUM)
+    ms = float(t.item())
+    j_step = float(joules.item())
+    value = B / (ms / 1e3)
+
+    # ---- dominant-kernel probe: the fused forward GEMM (local + decompress, bias+ReLU epilogue)
+    peak, peak_sus, hbm, peak_kind = peaks()
+    lmid = L // 2
+    probe_iters = 20
+    pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    import ctypes
+    lay = eng._layer(0, lmid, eng.parity)
+    y = eng.Y[eng.parity][0][lmid]
+    out = eng.Y[eng.parity][0][lmid + 1]
+    for _ in range(3):
+        eng.ctx.call("ppx_forward_update", eng.pdt, ctypes.byref(lay), B, eng.act.code, y.data_ptr(), eng.s,
+                     eng.G[lmid].data_ptr(), out.data_ptr(), eng.s, None, 0, S.cuda_stream)
+    pe0.record(S)
+    for _ in range(probe_iters):
+        eng.ctx.call("ppx_forward_update", eng.pdt, ctypes.byref(lay), B, eng.act.code, y.data_ptr(), eng.s,
+                     eng.G[lmid].data_ptr(), out.data_ptr(), eng.s, None, 0, S.cuda_stream)
+    pe1.record(S)
+    torch.cuda.synchronize()
+    k1_ms = pe0.elapsed_time(pe1) / probe_iters
+    s = n // p
+    k1_flops = 2 * B * s * (s + (p - 1) * k)
+    k1_tflops = k1_flops / (k1_ms / 1e3) / 1e12
+    step_flops = eng.R * pp_step_flops(n, p, k, L, B)
+    step_tflops = step_flops / (ms / 1e3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- end-to-end through the public API: pinned host batches, H2D + D2H(loss) in the timed region
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.stack([x.cpu() for x in xs]).pin_memory()
+        th = torch.stack([t_.cpu() for t_ in ts]).pin_memory()
+        h2d = 2 * xh.numel() * xh.element_size()
+        barrier()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record(S)
+        ready = eng.load_batch_async(xh, th, eng.parity)
+        for i in range(args.steps):
+            S.wait_event(ready)
+            par = eng.parity
+            eng.step(graph=use_graph)
+            done = torch.cuda.Event()
+            done.record(S)
+            eng.copy_stream.wait_event(done)            # next parity's buffers are free again
+            if i + 1 < args.steps:
+                ready = eng.load_batch_async(xh, th, 1 - par)
+            eng.read_loss()                              # D2H of the step's loss (+ non-finite flag)
+        q1.record(S)
+        barrier()
+        te = torch.tensor([q0.elapsed_time(q1) / args.steps], device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": B / (float(te.item()) / 1e3), "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": 8}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        sample_b, sample_l = 256, 1
+        try:
+            tcpu = cpu_sample(n, p, k, sample_l, sample_b)
+            cpu = {"value": sample_b / (tcpu * L / sample_l), "unit": "samples/s", "cores": cores, "kind": "port",
+                   "sample": f"oracle pp_iteration (float64, numpy/OpenBLAS) of ONE layer of the {args.config} model "
+                             f"(all {p} ranks) at batch {sample_b}, best of 2, scaled x{L // sample_l} layers"}
+        except Exception as exc:  # pragma: no cover
+            cpu = {"value": None, "unit": "samples/s", "cores": cores, "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"phantom FFN {args.config}: n={n}, L={L}, p={p} logical ranks, k={k}, "
+                                   f"batch {B}, ReLU, mean loss, SGD; {eng.R} logical rank(s) per GPU",
+                       "global_batch": B, "width": n, "layers": L, "p": p, "k": k,
+                       "parallelism": f"phantom pp{p} over {world} GPU(s)",
+                       "l2": "working set per step (weights + activations) exceeds the 126 MB L2; no flush",
+                       "graphs": use_graph},
+            "roofline": {"bound": "tensor", "achieved": k1_tflops, "peak": peak, "unit": "TFLOP/s",
+                         "frac": k1_tflops / peak, "traffic": traffic, "kernel": "fused forward GEMM (ppx_forward_update)",
+                         "flops_per_launch": k1_flops, "ms_per_launch": k1_ms, "peak_kind": f"{peak_kind} burst",
+                         "step_tflops_per_gpu": step_tflops, "step_frac_of_sustained": step_tflops / peak_sus},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+            "energy": {"j_per_step_all_gpus": j_step, "j_per_epoch": j_step * STEPS_PER_EPOCH,
+                       "epoch_samples": STEPS_PER_EPOCH * B},
+            "loss": {"after_warmup": loss0, "after_timed": loss1},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

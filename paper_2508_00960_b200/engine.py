@@ -107,7 +107,9 @@ class PhantomEngine:
             self.ctx.call("ppx_reserve_workspace", int(2 * 4 * per_call * 1.25) + (1 << 20))
         self.graphs = [None, None]
         self.parity = 0
-        self._keep = []   # ctypes structs referenced by captured launches
+        self._keep = []   # ctypes structs of the launch being built
+        self._launches = 0
+        self.launch_count = 0
 
     # ------------------------------------------------------------------------------------------
     def _init_weights(self, seed):
@@ -188,6 +190,15 @@ class PhantomEngine:
     def _received(self, l, j):
         return self.H[l].data_ptr() + j * self.B * self.off["ldk"] * self.H[l].element_size()
 
+    _KERNEL_CALLS = {"ppx_compress", "ppx_forward_update", "ppx_forward_output", "ppx_error_phantoms", "ppx_wgrad",
+                     "ppx_backward_delta", "ppx_optimizer_step"}
+
+    def _call(self, name, *args):
+        """ctx.call that counts the launches of our own kernels (NCCL / memsets excluded)."""
+        self.ctx.call(name, *args)
+        if name in self._KERNEL_CALLS:
+            self._launches += 1
+
     @staticmethod
     def _join(src: torch.cuda.Stream, dst: torch.cuda.Stream):
         ev = torch.cuda.Event()
@@ -200,22 +211,22 @@ class PhantomEngine:
         for l in range(self.L):
             for jj in range(self.R):
                 y = self.Y[par][jj][l]
-                c.call("ppx_compress", pdt, ctypes.byref(self._layer(jj, l, par)), B, y.data_ptr(), s,
+                self._call("ppx_compress", pdt, ctypes.byref(self._layer(jj, l, par)), B, y.data_ptr(), s,
                        self.G[l].data_ptr(), st)
             if self.world > 1:
                 self._join(S, self.comm_stream)
-                c.call("ppx_all_gather", pdt, self.G[l].data_ptr(), slot, self.R, self.comm_stream.cuda_stream)
+                self._call("ppx_all_gather", pdt, self.G[l].data_ptr(), slot, self.R, self.comm_stream.cuda_stream)
                 self._join(self.comm_stream, S)
             for jj in range(self.R):
                 y = self.Y[par][jj][l]
                 out = self.Y[par][jj][l + 1]
                 lay = ctypes.byref(self._layer(jj, l, par))
                 if l < self.L - 1 or not train:
-                    c.call("ppx_forward_update", pdt, lay, B, self.act.code, y.data_ptr(), s, self.G[l].data_ptr(),
+                    self._call("ppx_forward_update", pdt, lay, B, self.act.code, y.data_ptr(), s, self.G[l].data_ptr(),
                            out.data_ptr(), s, None, 0, st)
                 else:
                     mean = self.reduction == "mean"
-                    c.call("ppx_forward_output", pdt, lay, B, self.act.code, y.data_ptr(), s, self.G[l].data_ptr(),
+                    self._call("ppx_forward_output", pdt, lay, B, self.act.code, y.data_ptr(), s, self.G[l].data_ptr(),
                            out.data_ptr(), s, self.Tgt[par][jj].data_ptr(), s, self.D[jj][0].data_ptr(), s,
                            1.0 / B if mean else 1.0, 0.5 / B if mean else 0.5, self.loss.data_ptr(),
                            self.gbias[jj, l].data_ptr(), st)
@@ -227,13 +238,13 @@ class PhantomEngine:
         cur = 0
         for l in range(L - 1, -1, -1):
             if R > 1:  # several local ranks accumulate into the same contribution slots
-                c.call("ppx_zero", self.H[l].data_ptr(), self.H[l].numel() * esz, st)
+                self._call("ppx_zero", self.H[l].data_ptr(), self.H[l].numel() * esz, st)
             for jj in range(R):
-                c.call("ppx_error_phantoms", pdt, ctypes.byref(self._layer(jj, l, par)), B,
+                self._call("ppx_error_phantoms", pdt, ctypes.byref(self._layer(jj, l, par)), B,
                        self.D[jj][cur].data_ptr(), s, self.H[l].data_ptr(), int(R > 1), st)
             if self.world > 1:
                 self._join(S, self.comm_stream)
-                c.call("ppx_reduce_scatter", pdt, self.H[l].data_ptr(), slot, R, self.comm_stream.cuda_stream)
+                self._call("ppx_reduce_scatter", pdt, self.H[l].data_ptr(), slot, R, self.comm_stream.cuda_stream)
             # weight gradients that do not need r_l, overlapped with the reduce-scatter
             for jj in range(R):
                 j = self.local[jj]
@@ -247,14 +258,14 @@ class PhantomEngine:
                                                 ctypes.pointer(self._update(jj, l + 1, par))))
                 arr = (_lib.WgradItem * len(items))(*items)
                 self._keep.append(arr)
-                c.call("ppx_wgrad", pdt, len(items), arr, st)
+                self._call("ppx_wgrad", pdt, len(items), arr, st)
             if self.world > 1:
                 self._join(self.comm_stream, S)
             if l > 0:
                 for jj in range(R):
                     j = self.local[jj]
                     y_prev = self.Y[par][jj][l]
-                    c.call("ppx_backward_delta", pdt, ctypes.byref(self._layer(jj, l, par)), B, self.act.code,
+                    self._call("ppx_backward_delta", pdt, ctypes.byref(self._layer(jj, l, par)), B, self.act.code,
                            self.D[jj][cur].data_ptr(), s, self._received(l, j),
                            y_prev.data_ptr() if self.act is Activation.RELU else None, s,
                            self.D[jj][1 - cur].data_ptr(), s, self.gbias[jj, l - 1].data_ptr(), st)
@@ -266,23 +277,25 @@ class PhantomEngine:
                                     self._received(0, j), None, ctypes.pointer(self._update(jj, 0, par)))]
             arr = (_lib.WgradItem * 1)(*items)
             self._keep.append(arr)
-            c.call("ppx_wgrad", pdt, 1, arr, st)
+            self._call("ppx_wgrad", pdt, 1, arr, st)
         # biases of all local ranks and layers in one elementwise launch
         kind = _lib.PPX_UPDATE_ADAM if self.optimizer == "adam" else _lib.PPX_UPDATE_SGD
-        c.call("ppx_optimizer_step", kind, self.hyper.data_ptr(), self.bias.data_ptr(), self.gbias.data_ptr(),
+        self._call("ppx_optimizer_step", kind, self.hyper.data_ptr(), self.bias.data_ptr(), self.gbias.data_ptr(),
                self.adam_bm.data_ptr() if kind == _lib.PPX_UPDATE_ADAM else None,
                self.adam_bv.data_ptr() if kind == _lib.PPX_UPDATE_ADAM else None,
                self.bias.numel(), _lib.PPX_FP32, None, self.bad.data_ptr(), st)
 
     def _step_body(self, par, S):
         self._keep.clear()
+        self._launches = 0
         c, st = self.ctx, S.cuda_stream
-        c.call("ppx_zero", self.gbias.data_ptr(), self.gbias.numel() * 4, st)
-        c.call("ppx_zero", self.loss.data_ptr(), 4, st)
+        self._call("ppx_zero", self.gbias.data_ptr(), self.gbias.numel() * 4, st)
+        self._call("ppx_zero", self.loss.data_ptr(), 4, st)
         self._forward(par, S)
         self._backward(par, S)
         if self.world > 1:
-            c.call("ppx_all_reduce_f32", self.loss.data_ptr(), 1, st)
+            self._call("ppx_all_reduce_f32", self.loss.data_ptr(), 1, st)
+        self.launch_count = self._launches
 
     # ------------------------------------------------------------------------------------------
     def _set_hyper(self):
