@@ -135,6 +135,31 @@ ppx_status ppx_forward_output(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, in
                               void* delta, int64_t ld_d, float delta_scale, float loss_scale,
                               float* loss, float* bias_grad, void* stream);
 
+/* ---- grouped (multi-rank) launches: the logical ranks one GPU owns share ONE kernel launch,
+   so n small per-rank grids become one grid with n times the tiles (no wave-quantisation tail
+   per rank).  Each entry names one rank's operands; unused fields are NULL / 0. ------------- */
+typedef struct {
+  const ppx_layer* layer;
+  const void* x;       int64_t ld_x;    /* y_prev (compress / forward) or delta (backward) */
+  void* out;           int64_t ld_out;  /* y (forward) or delta_prev (backward) */
+  void* aux;           int64_t ld_aux;  /* forward: pre-activation (NULL: none); output layer: delta */
+  const void* target;  int64_t ld_t;    /* output layer: target */
+  const void* mask;    int64_t ld_m;    /* backward: ReLU' source (pre_prev or y_prev) */
+  const void* received;                 /* backward: [B, ldk] reduced phantom gradient */
+  float* colsum;                        /* output layer / backward: += batch sums of the delta */
+} ppx_rank_io;
+
+/* n x ppx_compress in one launch */
+ppx_status ppx_compress_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B,
+                          void* phantoms, void* stream);
+/* n x ppx_forward_update (output_layer = 0) or n x ppx_forward_output (output_layer = 1) */
+ppx_status ppx_forward_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B, ppx_act act,
+                         const void* phantoms, int32_t output_layer, float delta_scale, float loss_scale,
+                         float* loss, void* stream);
+/* n x ppx_backward_delta */
+ppx_status ppx_backward_delta_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B,
+                                ppx_act act_prev, void* stream);
+
 /* phantom.py:169-182 (+ training.py:66-69 scaling) — standalone output delta and loss partial.
    `pre` is the pre-activation (or the layer output: ReLU'(pre) == (y > 0)). */
 ppx_status ppx_output_delta(ppx_ctx* ctx, ppx_dtype dt, int32_t B, int32_t s, ppx_act act,

@@ -47,6 +47,13 @@ class WgradItem(ctypes.Structure):
                 ("upd", ctypes.POINTER(Update))]
 
 
+class RankIO(ctypes.Structure):
+    """ppx_rank_io: one logical rank's operands in a grouped launch."""
+    _fields_ = [("layer", ctypes.POINTER(Layer)), ("x", _vp), ("ld_x", _i64), ("out", _vp), ("ld_out", _i64),
+                ("aux", _vp), ("ld_aux", _i64), ("target", _vp), ("ld_t", _i64), ("mask", _vp), ("ld_m", _i64),
+                ("received", _vp), ("colsum", _vp)]
+
+
 GRAD_LOCAL, GRAD_COMP, GRAD_DEC, GRAD_BIAS, GRAD_ALL = 1, 2, 4, 8, 15
 
 
@@ -66,6 +73,9 @@ _SIGS = {
     "ppx_num_sms": (_i32, [_vp]),
     "ppx_reserve_workspace": (_i32, [_vp, _i64]),
     "ppx_compress": (_i32, [_vp, _i32, ctypes.POINTER(Layer), _i32, _vp, _i64, _vp, _vp]),
+    "ppx_compress_n": (_i32, [_vp, _i32, _i32, ctypes.POINTER(RankIO), _i32, _vp, _vp]),
+    "ppx_forward_n": (_i32, [_vp, _i32, _i32, ctypes.POINTER(RankIO), _i32, _i32, _vp, _i32, _f32, _f32, _fp, _vp]),
+    "ppx_backward_delta_n": (_i32, [_vp, _i32, _i32, ctypes.POINTER(RankIO), _i32, _i32, _vp]),
     "ppx_all_gather": (_i32, [_vp, _i32, _vp, _i64, _i32, _vp]),
     "ppx_forward_update": (_i32, [_vp, _i32, ctypes.POINTER(Layer), _i32, _i32, _vp, _i64, _vp,
                                   _vp, _i64, _vp, _i64, _vp]),

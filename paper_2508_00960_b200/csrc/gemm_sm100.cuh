@@ -38,8 +38,8 @@ constexpr int A_STAGE_BYTES = BM * ROW_BYTES;          // 16 KB
 constexpr int B_STAGE_BYTES = BN_MAX * ROW_BYTES;      // 32 KB
 constexpr int NUM_THREADS = 256;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 spare, w4-7 epilogue
 constexpr int TMEM_COLS = 512;    // 2 accumulator stages x 256 fp32 columns
-constexpr int MAX_MAPS = 24;
-constexpr int MAX_PROBS = 8;
+constexpr int MAX_MAPS = 40;
+constexpr int MAX_PROBS = 16;
 constexpr int MAX_SEGS = 6;
 constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
 
@@ -62,7 +62,7 @@ struct Operand {
   int8_t map;        // tensor-map index
   int8_t mn;         // 0 = K-major, 1 = MN-major
   int8_t slot_src;   // 0 = const, 1 = K-block index, 2 = N-block index
-  int8_t pad_;
+  int8_t atoms4d;    // MN-major only: map is 4D {atom, K, atoms, slots}; one TMA per stage
   int slot_base;
   int slot_skip;     // raw slot index >= skip is shifted by one (own rank excluded); INT_MAX = none
 };
@@ -163,6 +163,14 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint32_t bar
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
       "[%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint32_t bar, uint32_t dst, int c0, int c1,
+                                            int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
@@ -402,6 +410,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
             const int slot_b = op_slot(seg.b, kblk, tc.qn);
             if (!seg.a.mn) {
               tma_load_3d(ma, full_bar(stage), da, kin, tc.m0, slot_a);
+            } else if (seg.a.atoms4d) {
+              tma_load_4d(ma, full_bar(stage), da, 0, kin, tc.m0 / CH, slot_a);
             } else {
 #pragma unroll 1
               for (int c = 0; c < BM / CH; ++c)
@@ -409,6 +419,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
             }
             if (!seg.b.mn) {
               tma_load_3d(mb, full_bar(stage), db, kin, tc.nin, slot_b);
+            } else if (seg.b.atoms4d) {
+              tma_load_4d(mb, full_bar(stage), db, 0, kin, tc.nin / CH, slot_b);
             } else {
 #pragma unroll 1
               for (int c = 0; c < pr.BN / CH; ++c)

@@ -157,6 +157,8 @@ struct Builder {
     return r;
   }
 
+  bool use4d = getenv("PPX_NO_4D") == nullptr;
+
   Builder(ppx_ctx* c, ppx_dtype dt, void* stream) : ctx(c), st((cudaStream_t)stream), tf32(dt == PPX_FP32) {
     esize = tf32 ? 4 : 2;
     BK = ppx::ROW_BYTES / esize;
@@ -214,6 +216,28 @@ struct Builder {
     return P.nmaps++;
   }
 
+  // MN-major operand as ONE 4D box per stage: {CH elements, BK rows, atoms, 1} over the view
+  // re-indexed as [slots][atoms][rows][CH] (atom stride = CH elements). Needs cols % CH == 0.
+  int add_map4(const View& v, int atoms) {
+    if (!ok()) return 0;
+    MapKey key{v.ptr, v.cols, v.rows, v.slots, v.ld, v.slot_stride, -CH, atoms};
+    auto hit = map_cache.find(key);
+    if (hit != map_cache.end()) return hit->second;
+    if (P.nmaps >= ppx::MAX_MAPS) { error(PPX_E_CONFIG, "too many tensor maps in one launch"); return 0; }
+    if (!get_encode()) { error(PPX_E_CUDA, "cuTensorMapEncodeTiled unavailable"); return 0; }
+    cuuint64_t dims[4] = {(cuuint64_t)CH, (cuuint64_t)v.rows, (cuuint64_t)(v.cols / CH), (cuuint64_t)v.slots};
+    cuuint64_t strides[3] = {(cuuint64_t)(v.ld * esize), (cuuint64_t)(CH * esize), (cuuint64_t)(v.slot_stride * esize)};
+    cuuint32_t box[4] = {(cuuint32_t)CH, (cuuint32_t)BK, (cuuint32_t)atoms, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = g_encode(&P.maps[P.nmaps], tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                          4, const_cast<void*>(v.ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return -1;  // caller falls back to per-atom 3D boxes
+    map_cache[key] = P.nmaps;
+    return P.nmaps++;
+  }
+
   // FP32 tier: hi = tf32-truncated x, lo = x - hi over the whole strided extent of the view.
   // MN-major views are transposed while split and come back K-major (`mn` cleared).
   std::pair<View, View> split(const View& v, int& mn) {
@@ -251,38 +275,70 @@ struct Builder {
     return {hi, lo};
   }
 
+  struct PendingSeg {
+    Opnd a, b;
+    int k_tiles, kpb;
+  };
+  std::vector<PendingSeg> pend[ppx::MAX_PROBS];
+  bool prob_bmn[ppx::MAX_PROBS] = {};
+
+  static int pick_bn(int nb_extent, int gran) {
+    int ntiles = (int)cdiv(nb_extent, ppx::BN_MAX);
+    int bn = (int)cdiv(cdiv(nb_extent, ntiles), gran) * gran;
+    return bn > ppx::BN_MAX ? ppx::BN_MAX : bn;
+  }
+
   Problem* new_problem(int M, int nb_extent, int nblk, bool b_mn) {
     if (!ok()) return nullptr;
     if (P.nprobs >= ppx::MAX_PROBS) { error(PPX_E_CONFIG, "too many problems in one launch"); return nullptr; }
     if (M <= 0 || nb_extent <= 0 || nblk <= 0) { error(PPX_E_CONFIG, "empty GEMM problem"); return nullptr; }
-    Problem* pr = &P.probs[P.nprobs++];
+    const int idx = P.nprobs++;
+    Problem* pr = &P.probs[idx];
     memset(pr, 0, sizeof(*pr));
-    const int gran = b_mn ? CH : 16;
-    int ntiles = (int)cdiv(nb_extent, ppx::BN_MAX);
-    int bn = (int)cdiv(cdiv(nb_extent, ntiles), gran) * gran;
-    if (bn > ppx::BN_MAX) bn = ppx::BN_MAX;
+    pend[idx].clear();
+    prob_bmn[idx] = b_mn;
     pr->M = M;
     pr->nb_extent = nb_extent;
     pr->nblk = nblk;
-    pr->BN = bn;
+    pr->BN = pick_bn(nb_extent, b_mn ? CH : 16);
     pr->m_tiles = (int)cdiv(M, ppx::BM);
-    pr->npb = (int)cdiv(nb_extent, bn);
+    pr->npb = (int)cdiv(nb_extent, pr->BN);
     pr->epi.out_skip = INT_MAX;
     return pr;
   }
 
+  // record a K segment; tensor maps are built in launch() once every problem's BN is final
   void add_segment(Problem* pr, Opnd a, Opnd b, int k_tiles, int kpb) {
     if (!ok() || !pr) return;
     if (k_tiles <= 0) { error(PPX_E_CONFIG, "empty K segment"); return; }
+    pend[pr - P.probs].push_back({a, b, k_tiles, kpb});
+  }
+
+  void finalize(Problem* pr, const PendingSeg& ps) {
+    Opnd a = ps.a, b = ps.b;
+    const int k_tiles = ps.k_tiles, kpb = ps.kpb;
+    // an MN-major tile is loaded in whole 128-byte atoms: a partial atom would never complete
+    // the stage's transaction count
+    if (b.mn && !tf32 && pr->BN % CH) { error(PPX_E_CONFIG, "MN-major B tile width must be a multiple of 64"); return; }
     auto push = [&](const View& av, const View& bv) {
       if (pr->nsegs >= ppx::MAX_SEGS) { error(PPX_E_CONFIG, "too many K segments"); return; }
       Segment& s = pr->segs[pr->nsegs++];
-      s.a.map = (int8_t)(a.mn ? add_map(av, CH, BK) : add_map(av, BK, ppx::BM));
+      s.a.atoms4d = 0;
+      s.b.atoms4d = 0;
+      if (a.mn && use4d && av.cols % CH == 0) {
+        int m = add_map4(av, ppx::BM / CH);
+        if (m >= 0) { s.a.map = (int8_t)m; s.a.atoms4d = 1; }
+      }
+      if (!s.a.atoms4d) s.a.map = (int8_t)(a.mn ? add_map(av, CH, BK) : add_map(av, BK, ppx::BM));
       s.a.mn = (int8_t)a.mn;
       s.a.slot_src = (int8_t)a.slot_src;
       s.a.slot_base = a.slot_base;
       s.a.slot_skip = a.slot_skip;
-      s.b.map = (int8_t)(b.mn ? add_map(bv, CH, BK) : add_map(bv, BK, pr->BN));
+      if (b.mn && use4d && bv.cols % CH == 0 && pr->BN % CH == 0) {
+        int m = add_map4(bv, pr->BN / CH);
+        if (m >= 0) { s.b.map = (int8_t)m; s.b.atoms4d = 1; }
+      }
+      if (!s.b.atoms4d) s.b.map = (int8_t)(b.mn ? add_map(bv, CH, BK) : add_map(bv, BK, pr->BN));
       s.b.mn = (int8_t)b.mn;
       s.b.slot_src = (int8_t)b.slot_src;
       s.b.slot_base = b.slot_base;
@@ -304,6 +360,28 @@ struct Builder {
   }
 
   ppx_status launch() {
+    if (!ok()) return status;
+    auto count_tiles = [&]() {
+      int t = 0;
+      for (int i = 0; i < P.nprobs; ++i) t += P.probs[i].m_tiles * P.probs[i].nblk * P.probs[i].npb;
+      return t;
+    };
+    // small launches: trade N-tile width for more CTAs (tcgen05 throughput per SM is N-invariant)
+    for (int guard = 0; guard < 4 && count_tiles() * 4 < ctx->num_sms * 3; ++guard) {
+      bool changed = false;
+      for (int i = 0; i < P.nprobs; ++i) {
+        Problem& pr = P.probs[i];
+        const int gran = prob_bmn[i] ? CH : 32;
+        if (pr.BN / 2 >= gran && (pr.BN / 2) % gran == 0 && (pr.BN / 2) % 16 == 0 && pr.nb_extent > pr.BN / 2) {
+          pr.BN /= 2;
+          pr.npb = (int)cdiv(pr.nb_extent, pr.BN);
+          changed = true;
+        }
+      }
+      if (!changed) break;
+    }
+    for (int i = 0; i < P.nprobs && ok(); ++i)
+      for (const PendingSeg& ps : pend[i]) finalize(&P.probs[i], ps);
     if (!ok()) return status;
     int tiles = 0;
     for (int i = 0; i < P.nprobs; ++i) {
@@ -406,26 +484,49 @@ ppx_status ppx_reserve_workspace(ppx_ctx* ctx, int64_t bytes) {
 }
 
 // ---------------------------------------------------------------------------------------------
-ppx_status ppx_compress(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, const void* y_prev, int64_t ld_y,
-                        void* phantoms, void* stream) {
-  if (!ctx) return PPX_E_CONFIG;
-  if (bad_layer(L) || B < 1 || !y_prev || !phantoms) return fail(ctx, PPX_E_CONFIG, "ppx_compress: bad arguments");
+static ppx_status add_compress(ppx_ctx* ctx, ppx_dtype dt, Builder& b, const ppx_rank_io& io, int32_t B,
+                               void* phantoms) {
+  const ppx_layer* L = io.layer;
+  if (bad_layer(L) || B < 1 || !io.x || !phantoms) return fail(ctx, PPX_E_CONFIG, "compress: bad arguments");
   Flat f(L->s, L->k, L->p);
-  Builder b(ctx, dt, stream);
   Problem* pr = b.new_problem(B, L->k, 1, false);
-  Opnd a{view2(y_prev, B, L->s, ld_y)};
+  Opnd a{view2(io.x, B, L->s, io.ld_x)};
   Opnd w{view2(elem(dt, L->w, f.comp), L->k, L->s, f.lds)};
   b.add_segment(pr, a, w, (int)cdiv(L->s, b.BK), (int)cdiv(L->s, b.BK));
   if (pr) pr->epi.out = t2((char*)phantoms + (int64_t)L->rank * B * f.ldk * b.esize, f.ldk, dt == PPX_FP32);
+  return b.ok() ? PPX_OK : b.status;
+}
+
+ppx_status ppx_compress_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B, void* phantoms,
+                          void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (n < 1 || !io) return fail(ctx, PPX_E_CONFIG, "ppx_compress_n: bad arguments");
+  Builder b(ctx, dt, stream);
+  for (int i = 0; i < n; ++i) {
+    ppx_status s = add_compress(ctx, dt, b, io[i], B, phantoms);
+    if (s != PPX_OK) return s;
+  }
   return b.launch();
 }
 
-static ppx_status forward_common(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, ppx_act act,
-                                 const void* y_prev, int64_t ld_y, const void* phantoms, void* stream, Builder& b,
-                                 Problem*& pr) {
+ppx_status ppx_compress(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, const void* y_prev, int64_t ld_y,
+                        void* phantoms, void* stream) {
+  ppx_rank_io io{};
+  io.layer = L;
+  io.x = y_prev;
+  io.ld_x = ld_y;
+  return ppx_compress_n(ctx, dt, 1, &io, B, phantoms, stream);
+}
+
+static ppx_status add_forward(ppx_ctx* ctx, ppx_dtype dt, Builder& b, const ppx_rank_io& io, int32_t B, ppx_act act,
+                              const void* phantoms, int output_layer, float delta_scale, float loss_scale,
+                              float* loss) {
+  const ppx_layer* L = io.layer;
+  if (bad_layer(L) || B < 1 || !io.x || !io.out) return fail(ctx, PPX_E_CONFIG, "forward: bad arguments");
+  if (output_layer && (!io.target || !io.aux || !loss)) return fail(ctx, PPX_E_CONFIG, "forward output: bad arguments");
   Flat f(L->s, L->k, L->p);
-  pr = b.new_problem(B, L->s, 1, false);
-  Opnd a{view2(y_prev, B, L->s, ld_y)};
+  Problem* pr = b.new_problem(B, L->s, 1, false);
+  Opnd a{view2(io.x, B, L->s, io.ld_x)};
   Opnd w{view2(elem(dt, L->w, f.local), L->s, L->s, f.lds)};
   b.add_segment(pr, a, w, (int)cdiv(L->s, b.BK), (int)cdiv(L->s, b.BK));
   if (L->p > 1) {
@@ -438,52 +539,71 @@ static ppx_status forward_common(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L,
     int kpb = (int)cdiv(L->k, b.BK);
     b.add_segment(pr, g, d, kpb * (L->p - 1), kpb);
   }
-  if (pr) {
-    pr->epi.bias = L->bias ? L->bias : L->master + f.bias;
-    pr->epi.flags = ppx::EP_BIAS | (act == PPX_RELU ? ppx::EP_RELU : 0u);
+  if (!pr) return b.status;
+  const int f32 = dt == PPX_FP32;
+  pr->epi.bias = L->bias ? L->bias : L->master + f.bias;
+  pr->epi.flags = ppx::EP_BIAS | (act == PPX_RELU ? ppx::EP_RELU : 0u);
+  pr->epi.out = t2(io.out, io.ld_out, f32);
+  if (!output_layer) {
+    if (io.aux) {
+      pr->epi.flags |= ppx::EP_PREACT;
+      pr->epi.preact = t2(io.aux, io.ld_aux, f32);
+    }
+  } else {
+    pr->epi.flags |= ppx::EP_LOSS | (io.colsum ? ppx::EP_COLSUM : 0u);
+    pr->epi.aux = t2(io.aux, io.ld_aux, f32);
+    pr->epi.target = t2(const_cast<void*>(io.target), io.ld_t, f32);
+    pr->epi.scale = delta_scale;
+    pr->epi.loss_scale = loss_scale;
+    pr->epi.loss = loss;
+    pr->epi.colsum = io.colsum;
   }
   return b.ok() ? PPX_OK : b.status;
+}
+
+ppx_status ppx_forward_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B, ppx_act act,
+                         const void* phantoms, int32_t output_layer, float delta_scale, float loss_scale, float* loss,
+                         void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (n < 1 || !io) return fail(ctx, PPX_E_CONFIG, "ppx_forward_n: bad arguments");
+  Builder b(ctx, dt, stream);
+  for (int i = 0; i < n; ++i) {
+    ppx_status s = add_forward(ctx, dt, b, io[i], B, act, phantoms, output_layer, delta_scale, loss_scale, loss);
+    if (s != PPX_OK) return s;
+  }
+  return b.launch();
 }
 
 ppx_status ppx_forward_update(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, ppx_act act,
                               const void* y_prev, int64_t ld_y, const void* phantoms, void* y_out, int64_t ld_out,
                               void* preact, int64_t ld_pre, void* stream) {
-  if (!ctx) return PPX_E_CONFIG;
-  if (bad_layer(L) || B < 1 || !y_prev || !y_out) return fail(ctx, PPX_E_CONFIG, "ppx_forward_update: bad arguments");
-  Builder b(ctx, dt, stream);
-  Problem* pr = nullptr;
-  ppx_status s = forward_common(ctx, dt, L, B, act, y_prev, ld_y, phantoms, stream, b, pr);
-  if (s != PPX_OK) return s;
-  const int f32 = dt == PPX_FP32;
-  pr->epi.out = t2(y_out, ld_out, f32);
-  if (preact) {
-    pr->epi.flags |= ppx::EP_PREACT;
-    pr->epi.preact = t2(preact, ld_pre, f32);
-  }
-  return b.launch();
+  ppx_rank_io io{};
+  io.layer = L;
+  io.x = y_prev;
+  io.ld_x = ld_y;
+  io.out = y_out;
+  io.ld_out = ld_out;
+  io.aux = preact;
+  io.ld_aux = ld_pre;
+  return ppx_forward_n(ctx, dt, 1, &io, B, act, phantoms, 0, 1.f, 0.f, nullptr, stream);
 }
 
 ppx_status ppx_forward_output(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, ppx_act act,
                               const void* y_prev, int64_t ld_y, const void* phantoms, void* y_out, int64_t ld_out,
                               const void* target, int64_t ld_t, void* delta, int64_t ld_d, float delta_scale,
                               float loss_scale, float* loss, float* bias_grad, void* stream) {
-  if (!ctx) return PPX_E_CONFIG;
-  if (bad_layer(L) || B < 1 || !y_prev || !y_out || !target || !delta || !loss)
-    return fail(ctx, PPX_E_CONFIG, "ppx_forward_output: bad arguments");
-  Builder b(ctx, dt, stream);
-  Problem* pr = nullptr;
-  ppx_status s = forward_common(ctx, dt, L, B, act, y_prev, ld_y, phantoms, stream, b, pr);
-  if (s != PPX_OK) return s;
-  const int f32 = dt == PPX_FP32;
-  pr->epi.flags |= ppx::EP_LOSS | (bias_grad ? ppx::EP_COLSUM : 0u);
-  pr->epi.out = t2(y_out, ld_out, f32);
-  pr->epi.aux = t2(delta, ld_d, f32);
-  pr->epi.target = t2(const_cast<void*>(target), ld_t, f32);
-  pr->epi.scale = delta_scale;
-  pr->epi.loss_scale = loss_scale;
-  pr->epi.loss = loss;
-  pr->epi.colsum = bias_grad;
-  return b.launch();
+  ppx_rank_io io{};
+  io.layer = L;
+  io.x = y_prev;
+  io.ld_x = ld_y;
+  io.out = y_out;
+  io.ld_out = ld_out;
+  io.aux = delta;
+  io.ld_aux = ld_d;
+  io.target = target;
+  io.ld_t = ld_t;
+  io.colsum = bias_grad;
+  return ppx_forward_n(ctx, dt, 1, &io, B, act, phantoms, 1, delta_scale, loss_scale, loss, stream);
 }
 
 ppx_status ppx_output_delta(ppx_ctx* ctx, ppx_dtype dt, int32_t B, int32_t s, ppx_act act, const void* y_out,
@@ -668,39 +788,64 @@ ppx_status ppx_wgrad(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad
   return PPX_OK;
 }
 
-ppx_status ppx_backward_delta(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, ppx_act act_prev,
-                              const void* delta, int64_t ld_d, const void* received, const void* mask_src,
-                              int64_t ld_m, void* delta_prev, int64_t ld_dp, float* bias_grad_prev, void* stream) {
-  if (!ctx) return PPX_E_CONFIG;
-  if (bad_layer(L) || B < 1 || !delta || !delta_prev || (act_prev == PPX_RELU && !mask_src))
-    return fail(ctx, PPX_E_CONFIG, "ppx_backward_delta: bad arguments");
-  if (L->p > 1 && !received) return fail(ctx, PPX_E_SEQUENCING, "ppx_backward_delta: received gradient missing");
+static ppx_status add_backward(ppx_ctx* ctx, ppx_dtype dt, Builder& b, const ppx_rank_io& io, int32_t B,
+                               ppx_act act_prev) {
+  const ppx_layer* L = io.layer;
+  if (bad_layer(L) || B < 1 || !io.x || !io.out || (act_prev == PPX_RELU && !io.mask))
+    return fail(ctx, PPX_E_CONFIG, "backward_delta: bad arguments");
+  if (L->p > 1 && !io.received) return fail(ctx, PPX_E_SEQUENCING, "backward_delta: received gradient missing");
   Flat f(L->s, L->k, L->p);
-  Builder b(ctx, dt, stream);
   Problem* pr = b.new_problem(B, L->s, 1, true);
-  Opnd a{view2(delta, B, L->s, ld_d)};
+  Opnd a{view2(io.x, B, L->s, io.ld_x)};
   Opnd w{view2(elem(dt, L->w, f.local), L->s, L->s, f.lds)};
   w.mn = 1;
   b.add_segment(pr, a, w, (int)cdiv(L->s, b.BK), (int)cdiv(L->s, b.BK));
   if (L->p > 1) {
-    Opnd r{view2(received, B, L->k, f.ldk)};
+    Opnd r{view2(io.received, B, L->k, f.ldk)};
     Opnd c{view2(elem(dt, L->w, f.comp), L->k, L->s, f.lds)};
     c.mn = 1;
     b.add_segment(pr, r, c, (int)cdiv(L->k, b.BK), (int)cdiv(L->k, b.BK));
   }
-  if (pr) {
-    const int f32 = dt == PPX_FP32;
-    pr->epi.out = t2(delta_prev, ld_dp, f32);
-    if (act_prev == PPX_RELU) {
-      pr->epi.flags |= ppx::EP_MASK;
-      pr->epi.mask = t2(const_cast<void*>(mask_src), ld_m, f32);
-    }
-    if (bias_grad_prev) {
-      pr->epi.flags |= ppx::EP_COLSUM;
-      pr->epi.colsum = bias_grad_prev;
-    }
+  if (!pr) return b.status;
+  const int f32 = dt == PPX_FP32;
+  pr->epi.out = t2(io.out, io.ld_out, f32);
+  if (act_prev == PPX_RELU) {
+    pr->epi.flags |= ppx::EP_MASK;
+    pr->epi.mask = t2(const_cast<void*>(io.mask), io.ld_m, f32);
+  }
+  if (io.colsum) {
+    pr->epi.flags |= ppx::EP_COLSUM;
+    pr->epi.colsum = io.colsum;
+  }
+  return b.ok() ? PPX_OK : b.status;
+}
+
+ppx_status ppx_backward_delta_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B,
+                                ppx_act act_prev, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (n < 1 || !io) return fail(ctx, PPX_E_CONFIG, "ppx_backward_delta_n: bad arguments");
+  Builder b(ctx, dt, stream);
+  for (int i = 0; i < n; ++i) {
+    ppx_status s = add_backward(ctx, dt, b, io[i], B, act_prev);
+    if (s != PPX_OK) return s;
   }
   return b.launch();
+}
+
+ppx_status ppx_backward_delta(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, ppx_act act_prev,
+                              const void* delta, int64_t ld_d, const void* received, const void* mask_src,
+                              int64_t ld_m, void* delta_prev, int64_t ld_dp, float* bias_grad_prev, void* stream) {
+  ppx_rank_io io{};
+  io.layer = L;
+  io.x = delta;
+  io.ld_x = ld_d;
+  io.out = delta_prev;
+  io.ld_out = ld_dp;
+  io.mask = mask_src;
+  io.ld_m = ld_m;
+  io.received = received;
+  io.colsum = bias_grad_prev;
+  return ppx_backward_delta_n(ctx, dt, 1, &io, B, act_prev, stream);
 }
 
 ppx_status ppx_colsum(ppx_ctx* ctx, ppx_dtype dt, int32_t rows, int32_t cols, const void* x, int64_t ld, float* out,

@@ -191,7 +191,8 @@ class PhantomEngine:
         return self.H[l].data_ptr() + j * self.B * self.off["ldk"] * self.H[l].element_size()
 
     _KERNEL_CALLS = {"ppx_compress", "ppx_forward_update", "ppx_forward_output", "ppx_error_phantoms", "ppx_wgrad",
-                     "ppx_backward_delta", "ppx_optimizer_step"}
+                     "ppx_backward_delta", "ppx_optimizer_step", "ppx_compress_n", "ppx_forward_n",
+                     "ppx_backward_delta_n"}
 
     def _call(self, name, *args):
         """ctx.call that counts the launches of our own kernels (NCCL / memsets excluded)."""
@@ -205,34 +206,47 @@ class PhantomEngine:
         ev.record(src)
         dst.wait_event(ev)
 
+    def _io(self, jj, l, par, **kw):
+        io = _lib.RankIO()
+        io.layer = ctypes.pointer(self._layer(jj, l, par))
+        for k_, v in kw.items():
+            setattr(io, k_, v)
+        return io
+
+    def _ios(self, ios):
+        arr = (_lib.RankIO * len(ios))(*ios)
+        self._keep.append(arr)
+        return arr
+
     def _forward(self, par, S, train=True):
-        c, st, pdt, B, s = self.ctx, S.cuda_stream, self.pdt, self.B, self.s
+        st, pdt, B, s, R = S.cuda_stream, self.pdt, self.B, self.s, self.R
         slot = B * self.off["ldk"]
         for l in range(self.L):
-            for jj in range(self.R):
-                y = self.Y[par][jj][l]
-                self._call("ppx_compress", pdt, ctypes.byref(self._layer(jj, l, par)), B, y.data_ptr(), s,
-                       self.G[l].data_ptr(), st)
+            ios = [self._io(jj, l, par, x=self.Y[par][jj][l].data_ptr(), ld_x=s) for jj in range(R)]
+            self._call("ppx_compress_n", pdt, R, self._ios(ios), B, self.G[l].data_ptr(), st)
             if self.world > 1:
                 self._join(S, self.comm_stream)
-                self._call("ppx_all_gather", pdt, self.G[l].data_ptr(), slot, self.R, self.comm_stream.cuda_stream)
+                self._call("ppx_all_gather", pdt, self.G[l].data_ptr(), slot, R, self.comm_stream.cuda_stream)
                 self._join(self.comm_stream, S)
-            for jj in range(self.R):
-                y = self.Y[par][jj][l]
-                out = self.Y[par][jj][l + 1]
-                lay = ctypes.byref(self._layer(jj, l, par))
-                if l < self.L - 1 or not train:
-                    self._call("ppx_forward_update", pdt, lay, B, self.act.code, y.data_ptr(), s, self.G[l].data_ptr(),
-                           out.data_ptr(), s, None, 0, st)
-                else:
-                    mean = self.reduction == "mean"
-                    self._call("ppx_forward_output", pdt, lay, B, self.act.code, y.data_ptr(), s, self.G[l].data_ptr(),
-                           out.data_ptr(), s, self.Tgt[par][jj].data_ptr(), s, self.D[jj][0].data_ptr(), s,
-                           1.0 / B if mean else 1.0, 0.5 / B if mean else 0.5, self.loss.data_ptr(),
-                           self.gbias[jj, l].data_ptr(), st)
+            last = train and l == self.L - 1
+            ios = []
+            for jj in range(R):
+                kw = dict(x=self.Y[par][jj][l].data_ptr(), ld_x=s, out=self.Y[par][jj][l + 1].data_ptr(), ld_out=s)
+                if last:
+                    kw.update(aux=self.D[jj][0].data_ptr(), ld_aux=s, target=self.Tgt[par][jj].data_ptr(), ld_t=s,
+                              colsum=self.gbias[jj, l].data_ptr())
+                ios.append(self._io(jj, l, par, **kw))
+            mean = self.reduction == "mean"
+            self._call("ppx_forward_n", pdt, R, self._ios(ios), B, self.act.code, self.G[l].data_ptr(), int(last),
+                       1.0 / B if mean else 1.0, 0.5 / B if mean else 0.5, self.loss.data_ptr() if last else None, st)
+
+    def _launch_wgrad(self, items, st):
+        arr = (_lib.WgradItem * len(items))(*items)
+        self._keep.append(arr)
+        self._call("ppx_wgrad", self.pdt, len(items), arr, st)
 
     def _backward(self, par, S):
-        c, st, pdt, B, s, R, L = self.ctx, S.cuda_stream, self.pdt, self.B, self.s, self.R, self.L
+        st, pdt, B, s, R, L = S.cuda_stream, self.pdt, self.B, self.s, self.R, self.L
         slot = B * self.off["ldk"]
         esz = self.H[0].element_size()
         cur = 0
@@ -241,11 +255,12 @@ class PhantomEngine:
                 self._call("ppx_zero", self.H[l].data_ptr(), self.H[l].numel() * esz, st)
             for jj in range(R):
                 self._call("ppx_error_phantoms", pdt, ctypes.byref(self._layer(jj, l, par)), B,
-                       self.D[jj][cur].data_ptr(), s, self.H[l].data_ptr(), int(R > 1), st)
+                           self.D[jj][cur].data_ptr(), s, self.H[l].data_ptr(), int(R > 1), st)
             if self.world > 1:
                 self._join(S, self.comm_stream)
                 self._call("ppx_reduce_scatter", pdt, self.H[l].data_ptr(), slot, R, self.comm_stream.cuda_stream)
             # weight gradients that do not need r_l, overlapped with the reduce-scatter
+            per_rank = []
             for jj in range(R):
                 j = self.local[jj]
                 items = [_lib.WgradItem(ctypes.pointer(self._layer(jj, l, par)), _lib.GRAD_LOCAL | _lib.GRAD_DEC, B,
@@ -256,34 +271,39 @@ class PhantomEngine:
                                                 self.D[jj][cur].data_ptr(), s, self.Y[par][jj][l + 1].data_ptr(), s,
                                                 None, self._received(l + 1, j), None,
                                                 ctypes.pointer(self._update(jj, l + 1, par))))
-                arr = (_lib.WgradItem * len(items))(*items)
-                self._keep.append(arr)
-                self._call("ppx_wgrad", pdt, len(items), arr, st)
+                per_rank.append(items)
+            nprob = 2 + (1 if l < L - 1 else 0) if self.p > 1 else 1
+            per = max(1, 16 // nprob)
+            nl = -(-R // per)
+            per = -(-R // nl)
+            for c in range(0, R, per):
+                self._launch_wgrad([it for chunk in per_rank[c:c + per] for it in chunk], st)
             if self.world > 1:
                 self._join(self.comm_stream, S)
             if l > 0:
+                ios = []
                 for jj in range(R):
                     j = self.local[jj]
-                    y_prev = self.Y[par][jj][l]
-                    self._call("ppx_backward_delta", pdt, ctypes.byref(self._layer(jj, l, par)), B, self.act.code,
-                           self.D[jj][cur].data_ptr(), s, self._received(l, j),
-                           y_prev.data_ptr() if self.act is Activation.RELU else None, s,
-                           self.D[jj][1 - cur].data_ptr(), s, self.gbias[jj, l - 1].data_ptr(), st)
+                    ios.append(self._io(jj, l, par, x=self.D[jj][cur].data_ptr(), ld_x=s,
+                                        out=self.D[jj][1 - cur].data_ptr(), ld_out=s,
+                                        mask=self.Y[par][jj][l].data_ptr() if self.act is Activation.RELU else None,
+                                        ld_m=s, received=self._received(l, j),
+                                        colsum=self.gbias[jj, l - 1].data_ptr()))
+                self._call("ppx_backward_delta_n", pdt, R, self._ios(ios), B, self.act.code, st)
                 cur = 1 - cur
-        for jj in range(R):   # d compressor of layer 0
-            j = self.local[jj]
-            items = [_lib.WgradItem(ctypes.pointer(self._layer(jj, 0, par)), _lib.GRAD_COMP, B,
-                                    self.D[jj][cur].data_ptr(), s, self.Y[par][jj][0].data_ptr(), s, None,
-                                    self._received(0, j), None, ctypes.pointer(self._update(jj, 0, par)))]
-            arr = (_lib.WgradItem * 1)(*items)
-            self._keep.append(arr)
-            self._call("ppx_wgrad", pdt, 1, arr, st)
+        # d compressor of layer 0, all local ranks in one launch
+        items = [_lib.WgradItem(ctypes.pointer(self._layer(jj, 0, par)), _lib.GRAD_COMP, B,
+                                self.D[jj][cur].data_ptr(), s, self.Y[par][jj][0].data_ptr(), s, None,
+                                self._received(0, self.local[jj]), None, ctypes.pointer(self._update(jj, 0, par)))
+                 for jj in range(R)]
+        if self.p > 1:
+            self._launch_wgrad(items, st)
         # biases of all local ranks and layers in one elementwise launch
         kind = _lib.PPX_UPDATE_ADAM if self.optimizer == "adam" else _lib.PPX_UPDATE_SGD
         self._call("ppx_optimizer_step", kind, self.hyper.data_ptr(), self.bias.data_ptr(), self.gbias.data_ptr(),
-               self.adam_bm.data_ptr() if kind == _lib.PPX_UPDATE_ADAM else None,
-               self.adam_bv.data_ptr() if kind == _lib.PPX_UPDATE_ADAM else None,
-               self.bias.numel(), _lib.PPX_FP32, None, self.bad.data_ptr(), st)
+                   self.adam_bm.data_ptr() if kind == _lib.PPX_UPDATE_ADAM else None,
+                   self.adam_bv.data_ptr() if kind == _lib.PPX_UPDATE_ADAM else None,
+                   self.bias.numel(), _lib.PPX_FP32, None, self.bad.data_ptr(), st)
 
     def _step_body(self, par, S):
         self._keep.clear()
