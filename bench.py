@@ -255,6 +255,8 @@ def main():
     use_graph = not args.no_graph
 
     def barrier():
+        # drain our own NCCL work first: two communicators' kernels must never interleave
+        torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -393,8 +395,17 @@ def main():
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        # tear down our NCCL communicator at the same point on every rank, then torch's
+        barrier()
+        print('[teardown] closing engine', file=sys.stderr, flush=True)
+        eng.close()
+        print('[teardown] engine closed', file=sys.stderr, flush=True)
         dist.barrier()
         dist.destroy_process_group()
+        print('[teardown] pg destroyed', file=sys.stderr, flush=True)
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
     return 0
 
 

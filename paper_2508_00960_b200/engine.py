@@ -27,6 +27,7 @@ import torch
 from . import _lib, kernels
 from .core import Activation, as_activation, flat_offsets, round8
 from .errors import ConfigurationError, TrainingError
+from .schedule import local_ranks
 
 
 def pp_step_flops(n: int, p: int, k: int, layers: int, batch: int) -> int:
@@ -57,7 +58,7 @@ class PhantomEngine:
             raise ConfigurationError("optimizer must be sgd or adam")
         self.n, self.p, self.k, self.L, self.B, self.s = n, p, k, layers, batch, s
         self.world, self.rank, self.R = world, rank, p // world
-        self.local = list(range(rank * self.R, (rank + 1) * self.R))
+        self.local = local_ranks(p, world, rank)
         self.act = as_activation(activation)
         self.reduction, self.optimizer, self.lr, self.betas, self.eps = reduction, optimizer, lr, betas, eps
         self.dtype = dtype
@@ -346,6 +347,17 @@ class PhantomEngine:
                 self._step_body(par, torch.cuda.current_stream())
             self.graphs[par] = g
         torch.cuda.synchronize()
+
+    def close(self):
+        """Release the CUDA graphs (they hold NCCL work) and then this GPU's communicator.
+        Call on every rank at the same point of the program."""
+        torch.cuda.synchronize()
+        for g in self.graphs:
+            if g is not None:
+                g.reset()
+        self.graphs = [None, None]
+        torch.cuda.synchronize()
+        self.ctx.close()
 
     def forward_only(self, par=None):
         """Inference (config C5): the forward loop without tape, loss or delta."""
