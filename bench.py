@@ -210,6 +210,77 @@ def make_data(eng, seed, cfg):
     return xs, ts
 
 
+def run_tp(args, cfg, world, rank, local_rank, uid, eng, xs, barrier, dist):
+    """The same-width Megatron tensor-parallel FFN (TPEngine) on the same GPUs, same batch."""
+    import torch
+    from paper_2508_00960_b200 import _lib, kernels
+    from paper_2508_00960_b200.schedule import tp_comm_bytes_per_step
+    from paper_2508_00960_b200.tensor_parallel import TPEngine, tp_step_flops
+    n, L, B = cfg["n"], cfg["layers"], cfg["batch"]
+    # full replicated input / teacher targets of the dense-width task
+    g = torch.Generator(device=eng.dev)
+    g.manual_seed(1234)
+    X = torch.randn((B, n), generator=g, device=eng.dev).to(torch.bfloat16)
+    Xr = torch.empty_like(X)
+    eng.ctx.call("ppx_bias_act", eng.pdt, B, n, X.data_ptr(), n, None, 0, Xr.data_ptr(), n,
+                 torch.cuda.current_stream().cuda_stream)
+    gt = torch.Generator(device=eng.dev)
+    gt.manual_seed(99)
+    W = (torch.randn((n, n), generator=gt, device=eng.dev) / n ** 0.5).to(torch.bfloat16)
+    T = kernels.gemm(Xr, W, transpose_b=True, out_dtype=torch.bfloat16, relu=True, ctx=eng.ctx)
+    del W, Xr
+    eng.close()                      # free the phantom engine's graphs + communicator first
+    torch.cuda.empty_cache()
+    tpe = TPEngine(n, L, B, world=world, rank=rank, device=local_rank,
+                   uid=uid if world == 1 else _shared_uid(rank, world, dist), lr=3e-6, dtype=torch.bfloat16)
+    tpe.set_batch(X, T, 0)
+    tpe.set_batch(X, T, 1)
+    del X, T
+    tpe.step(graph=False)
+    tpe.read_loss()
+    tpe.capture()
+    for _ in range(2):
+        tpe.step()
+    tpe.read_loss()
+    barrier()
+    e0 = energy_mj(local_rank)
+    S = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(3, min(args.steps, 10))
+    ev0.record(S)
+    for _ in range(steps):
+        tpe.step()
+    ev1.record(S)
+    barrier()
+    e1 = energy_mj(local_rank)
+    t = torch.tensor([ev0.elapsed_time(ev1) / steps], device="cuda")
+    j = torch.tensor([((e1 - e0) / 1e3 / steps) if (e0 is not None and e1 is not None) else float("nan")],
+                     device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(j, op=dist.ReduceOp.SUM)
+    ms = float(t.item())
+    loss = tpe.read_loss()
+    flops = tp_step_flops(n, world, L, B)
+    out = {"pipeline": f"Megatron tensor-parallel FFN n={n}, L={L}, batch {B}, column/row pairs, "
+                       f"{world} GPU(s), same kernels, SGD fused", "value": B / (ms / 1e3), "unit": "samples/s",
+           "ms_per_step": ms, "steps": steps, "step_tflops_per_gpu": flops / (ms / 1e3) / 1e12,
+           "j_per_step_all_gpus": float(j.item()), "j_per_epoch": float(j.item()) * STEPS_PER_EPOCH,
+           "comm_bytes_per_step_per_gpu": tp_comm_bytes_per_step(n, L, B, world), "loss": loss,
+           "gpu_launches": tpe.launch_count * steps}
+    if world > 1:
+        barrier()
+    tpe.close()
+    return out
+
+
+def _shared_uid(rank, world, dist):
+    from paper_2508_00960_b200 import _lib
+    uid = [_lib.Context.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    return uid[0]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -221,6 +292,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-tp", action="store_true")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.batch:
@@ -232,6 +304,7 @@ def main():
     import torch.distributed as dist
     from paper_2508_00960_b200 import _lib
     from paper_2508_00960_b200.engine import PhantomEngine, pp_step_flops
+    from paper_2508_00960_b200.schedule import comm_bytes_per_step
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -370,6 +443,10 @@ def main():
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": "samples/s", "cores": cores, "kind": "port", "sample": f"failed: {exc}"}
 
+    tp = None
+    if not args.no_tp and L % 2 == 0:
+        tp = run_tp(args, cfg, world, rank, local_rank, uid, eng, xs, barrier, dist)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
@@ -392,17 +469,22 @@ def main():
             "energy": {"j_per_step_all_gpus": j_step, "j_per_epoch": j_step * STEPS_PER_EPOCH,
                        "epoch_samples": STEPS_PER_EPOCH * B},
             "loss": {"after_warmup": loss0, "after_timed": loss1},
+            "comm_bytes_per_step_per_gpu": comm_bytes_per_step(n, p, k, L, B, world),
+            "tp": tp,
         }
+        if tp and tp.get("value"):
+            line["pp_vs_tp"] = {"speedup": value / tp["value"],
+                                "comm_bytes_ratio": (line["comm_bytes_per_step_per_gpu"] / tp["comm_bytes_per_step_per_gpu"]
+                                                     if tp["comm_bytes_per_step_per_gpu"] else None),
+                                "energy_per_epoch_ratio": (j_step / tp["j_per_step_all_gpus"]
+                                                           if tp.get("j_per_step_all_gpus") else None)}
         print(json.dumps(line), flush=True)
     if world > 1:
         # tear down our NCCL communicator at the same point on every rank, then torch's
         barrier()
-        print('[teardown] closing engine', file=sys.stderr, flush=True)
         eng.close()
-        print('[teardown] engine closed', file=sys.stderr, flush=True)
         dist.barrier()
         dist.destroy_process_group()
-        print('[teardown] pg destroyed', file=sys.stderr, flush=True)
         sys.stdout.flush()
         sys.stderr.flush()
         os._exit(0)

@@ -239,6 +239,13 @@ ppx_status ppx_gemm(ppx_ctx* ctx, ppx_dtype dt, int32_t M, int32_t N, int32_t K,
                     int32_t trans_b, void* c, int64_t ldc, ppx_dtype out_dt,
                     const ppx_epilogue* epi, void* stream);
 
+/* Weight-gradient GEMM with the optimizer fused into its epilogue (the Megatron TP comparison
+   pipeline): G = op(a) . op(b) [M, N] is applied to the fp32 master (leading dim ld_w) by
+   SGD / Adam and the new weights are written to upd->w_next in `dt`. */
+ppx_status ppx_gemm_update(ppx_ctx* ctx, ppx_dtype dt, int32_t M, int32_t N, int32_t K,
+                           const void* a, int64_t lda, int32_t trans_a, const void* b, int64_t ldb,
+                           int32_t trans_b, const ppx_update* upd, int64_t ld_w, void* stream);
+
 /* elementwise helpers used by the host engine */
 ppx_status ppx_zero(ppx_ctx* ctx, void* ptr, int64_t bytes, void* stream); /* cudaMemsetAsync */
 ppx_status ppx_cast(ppx_ctx* ctx, ppx_dtype src_dt, const void* src, ppx_dtype dst_dt, void* dst,

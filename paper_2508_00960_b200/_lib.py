@@ -96,6 +96,8 @@ _SIGS = {
     "ppx_optimizer_step": (_i32, [_vp, _i32, _fp, _fp, _fp, _fp, _fp, _i64, _i32, _vp, _vp, _vp]),
     "ppx_gemm": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _i64, _i32, _vp, _i64,
                         _i32, ctypes.POINTER(Epilogue), _vp]),
+    "ppx_gemm_update": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _i64, _i32,
+                               ctypes.POINTER(Update), _i64, _vp]),
     "ppx_zero": (_i32, [_vp, _vp, _i64, _vp]),
     "ppx_cast": (_i32, [_vp, _i32, _vp, _i32, _vp, _i64, _vp]),
     "ppx_bias_act": (_i32, [_vp, _i32, _i32, _i32, _vp, _i64, _fp, _i32, _vp, _i64, _vp]),

@@ -898,6 +898,26 @@ ppx_status ppx_gemm(ppx_ctx* ctx, ppx_dtype dt, int32_t M, int32_t N, int32_t K,
   return b.launch();
 }
 
+ppx_status ppx_gemm_update(ppx_ctx* ctx, ppx_dtype dt, int32_t M, int32_t N, int32_t K, const void* a, int64_t lda,
+                           int32_t trans_a, const void* bm, int64_t ldb, int32_t trans_b, const ppx_update* upd,
+                           int64_t ld_w, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (M < 1 || N < 1 || K < 1 || !a || !bm || !upd || upd->kind == PPX_UPDATE_NONE || !upd->master || !upd->hyper ||
+      (upd->kind == PPX_UPDATE_ADAM && (!upd->adam_m || !upd->adam_v)))
+    return fail(ctx, PPX_E_CONFIG, "ppx_gemm_update: bad arguments");
+  Builder b(ctx, dt, stream);
+  const bool b_mn = !trans_b;
+  Problem* pr = b.new_problem(M, N, 1, b_mn);
+  Opnd A{trans_a ? view2(a, K, M, lda) : view2(a, M, K, lda)};
+  A.mn = trans_a ? 1 : 0;
+  Opnd Bo{trans_b ? view2(bm, N, K, ldb) : view2(bm, K, N, ldb)};
+  Bo.mn = b_mn ? 1 : 0;
+  int kt = (int)cdiv(K, b.BK);
+  b.add_segment(pr, A, Bo, kt, kt);
+  if (pr) set_update(pr->epi, upd, dt, 0, ld_w, 0);
+  return b.launch();
+}
+
 ppx_status ppx_zero(ppx_ctx* ctx, void* ptr, int64_t bytes, void* stream) {
   if (!ctx) return PPX_E_CONFIG;
   if (bytes < 0 || (bytes > 0 && !ptr)) return fail(ctx, PPX_E_CONFIG, "ppx_zero: bad arguments");

@@ -350,7 +350,9 @@ class PhantomEngine:
 
     def close(self):
         """Release the CUDA graphs (they hold NCCL work) and then this GPU's communicator.
-        Call on every rank at the same point of the program."""
+        Call on every rank at the same point of the program (idempotent)."""
+        if self.ctx.handle is None:
+            return
         torch.cuda.synchronize()
         for g in self.graphs:
             if g is not None:
