@@ -211,6 +211,8 @@ typedef struct {
   const void* received;
   float* grad;
   const ppx_update* upd;
+  int32_t phantom_halves;   /* 0/1: phantoms is [p][B, ldk]; 2: two batch halves [2][p][B/2, ldk]
+                               (the engine all-gathers each half separately to overlap it) */
 } ppx_wgrad_item;
 ppx_status ppx_wgrad(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad_item* items, void* stream);
 

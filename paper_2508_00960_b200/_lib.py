@@ -44,7 +44,7 @@ class WgradItem(ctypes.Structure):
     """ppx_wgrad_item: one layer's weight-gradient request in a grouped launch."""
     _fields_ = [("layer", ctypes.POINTER(Layer)), ("parts", _i32), ("B", _i32), ("delta", _vp), ("ld_d", _i64),
                 ("y_prev", _vp), ("ld_y", _i64), ("phantoms", _vp), ("received", _vp), ("grad", _vp),
-                ("upd", ctypes.POINTER(Update))]
+                ("upd", ctypes.POINTER(Update)), ("phantom_halves", _i32)]
 
 
 class RankIO(ctypes.Structure):

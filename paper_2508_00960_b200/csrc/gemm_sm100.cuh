@@ -62,7 +62,8 @@ struct Operand {
   int8_t map;        // tensor-map index
   int8_t mn;         // 0 = K-major, 1 = MN-major
   int8_t slot_src;   // 0 = const, 1 = K-block index, 2 = N-block index
-  int8_t atoms4d;    // MN-major only: map is 4D {atom, K, atoms, slots}; one TMA per stage
+  int8_t atoms4d;    // MN-major only: 1 = 4D map {atom, K, atoms, slots} (atom-major smem tile);
+                     // 2 = 5D map {atom, 8 rows, atoms, K groups, slots}: canonical interleaved tile
   int slot_base;
   int slot_skip;     // raw slot index >= skip is shifted by one (own rank excluded); INT_MAX = none
 };
@@ -171,6 +172,14 @@ __device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint32_t bar
       "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
       "[%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(const CUtensorMap* map, uint32_t bar, uint32_t dst, int c2, int c3,
+                                            int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %3, %4, %5, %6}], "
+      "[%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(0), "r"(c2), "r"(c3), "r"(c4)
       : "memory");
 }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
@@ -410,6 +419,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
             const int slot_b = op_slot(seg.b, kblk, tc.qn);
             if (!seg.a.mn) {
               tma_load_3d(ma, full_bar(stage), da, kin, tc.m0, slot_a);
+            } else if (seg.a.atoms4d == 2) {
+              tma_load_5d(ma, full_bar(stage), da, tc.m0 / CH, kin / 8, slot_a);
             } else if (seg.a.atoms4d) {
               tma_load_4d(ma, full_bar(stage), da, 0, kin, tc.m0 / CH, slot_a);
             } else {
@@ -456,8 +467,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
             const uint32_t db = sB + stage * B_STAGE_BYTES;
 #pragma unroll
             for (int kk = 0; kk < NK; ++kk) {
-              uint64_t ad = seg.a.mn ? sdesc(da + kk * (KMMA * ROW_BYTES), BK * ROW_BYTES, 1024)
-                                     : sdesc(da + kk * 32, 16, 1024);
+              // MN-major A: atom-major tile (LBO = atom stride, SBO = 1024) or the interleaved
+              // canonical tile (LBO = 1024 between MN atoms, SBO = 2 KB between 8-row K groups)
+              uint64_t ad = !seg.a.mn ? sdesc(da + kk * 32, 16, 1024)
+                            : (seg.a.atoms4d == 2 ? sdesc(da + kk * (KMMA / 8) * (BM / CH) * 1024, 1024, (BM / CH) * 1024)
+                                                  : sdesc(da + kk * (KMMA * ROW_BYTES), BK * ROW_BYTES, 1024));
               uint64_t bd = seg.b.mn ? sdesc(db + kk * (KMMA * ROW_BYTES), BK * ROW_BYTES, 1024)
                                      : sdesc(db + kk * 32, 16, 1024);
               mma_issue<kTF32>(tmem_d, ad, bd, seg.idesc, accum);

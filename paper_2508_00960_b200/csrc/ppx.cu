@@ -158,6 +158,8 @@ struct Builder {
   }
 
   bool use4d = getenv("PPX_NO_4D") == nullptr;
+  // MN-major A (activations / deltas of the weight-gradient GEMMs) as the interleaved 5D tile
+  bool use5d = getenv("PPX_NO_5D") == nullptr;
 
   Builder(ppx_ctx* c, ppx_dtype dt, void* stream) : ctx(c), st((cudaStream_t)stream), tf32(dt == PPX_FP32) {
     esize = tf32 ? 4 : 2;
@@ -234,6 +236,30 @@ struct Builder {
                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return -1;  // caller falls back to per-atom 3D boxes
+    map_cache[key] = P.nmaps;
+    return P.nmaps++;
+  }
+
+  // MN-major A operand in the canonical interleaved SW128 order: ONE 5D box per stage,
+  // {CH elements, 8 rows, atoms, BK/8 groups, 1} over [slots][K groups][8 rows][atoms][CH]
+  int add_map5(const View& v, int atoms) {
+    if (!ok()) return 0;
+    MapKey key{v.ptr, v.cols, v.rows, v.slots, v.ld, v.slot_stride, -2 * CH, atoms};
+    auto hit = map_cache.find(key);
+    if (hit != map_cache.end()) return hit->second;
+    if (v.rows % 8) return -1;
+    if (P.nmaps >= ppx::MAX_MAPS) { error(PPX_E_CONFIG, "too many tensor maps in one launch"); return 0; }
+    if (!get_encode()) { error(PPX_E_CUDA, "cuTensorMapEncodeTiled unavailable"); return 0; }
+    cuuint64_t dims[5] = {(cuuint64_t)CH, 8, (cuuint64_t)(v.cols / CH), (cuuint64_t)(v.rows / 8), (cuuint64_t)v.slots};
+    cuuint64_t strides[4] = {(cuuint64_t)(v.ld * esize), (cuuint64_t)(CH * esize), (cuuint64_t)(8 * v.ld * esize),
+                             (cuuint64_t)(v.slot_stride * esize)};
+    cuuint32_t box[5] = {(cuuint32_t)CH, 8, (cuuint32_t)atoms, (cuuint32_t)(BK / 8), 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = g_encode(&P.maps[P.nmaps], tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                          5, const_cast<void*>(v.ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return -1;
     map_cache[key] = P.nmaps;
     return P.nmaps++;
   }
@@ -325,7 +351,11 @@ struct Builder {
       Segment& s = pr->segs[pr->nsegs++];
       s.a.atoms4d = 0;
       s.b.atoms4d = 0;
-      if (a.mn && use4d && av.cols % CH == 0) {
+      if (a.mn && use5d && av.cols % CH == 0) {
+        int m = add_map5(av, ppx::BM / CH);
+        if (m >= 0) { s.a.map = (int8_t)m; s.a.atoms4d = 2; }
+      }
+      if (a.mn && !s.a.atoms4d && use4d && av.cols % CH == 0) {
         int m = add_map4(av, ppx::BM / CH);
         if (m >= 0) { s.a.map = (int8_t)m; s.a.atoms4d = 1; }
       }
@@ -740,13 +770,21 @@ static ppx_status wgrad_add(ppx_ctx* ctx, ppx_dtype dt, Builder& b, const ppx_wg
   }
   if (need_g) {  // d decompressor_q = delta^T g_{src(q)}   [p-1][s, k]
     Problem* pd = b.new_problem(L->s, L->k, L->p - 1, true);
-    Opnd a{view2(it.delta, B, L->s, it.ld_d)};
-    a.mn = 1;
-    Opnd g{view3(it.phantoms, L->p, B, L->k, f.ldk, (int64_t)B * f.ldk)};
-    g.mn = 1;
-    g.slot_src = 2;
-    g.slot_skip = L->rank;
-    b.add_segment(pd, a, g, kt, kt);
+    const int H = it.phantom_halves == 2 ? 2 : 1;
+    if (B % H) return fail(ctx, PPX_E_CONFIG, "param grads: batch not divisible into phantom halves");
+    const int Bh = B / H;
+    const int es = dt == PPX_FP32 ? 4 : 2;
+    for (int h = 0; h < H; ++h) {   // the batch (K) splits into one segment per gathered half
+      Opnd a{view2(elem(dt, it.delta, (int64_t)h * Bh * it.ld_d), Bh, L->s, it.ld_d)};
+      a.mn = 1;
+      Opnd g{view3((const char*)it.phantoms + (int64_t)h * L->p * Bh * f.ldk * es, L->p, Bh, L->k, f.ldk,
+                   (int64_t)Bh * f.ldk)};
+      g.mn = 1;
+      g.slot_src = 2;
+      g.slot_skip = L->rank;
+      const int kth = (int)cdiv(Bh, b.BK);
+      b.add_segment(pd, a, g, kth, kth);
+    }
     if (pd) {
       if (update) set_update(pd->epi, upd, dt, f.dec, f.ldk, (int64_t)L->s * f.ldk);
       else pd->epi.out = t2(grad + f.dec, f.ldk, 1, (int64_t)L->s * f.ldk);
@@ -767,7 +805,7 @@ ppx_status ppx_param_grads(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32
                            const void* received, float* grad, const ppx_update* upd, int32_t parts,
                            void* stream) {
   if (!ctx) return PPX_E_CONFIG;
-  ppx_wgrad_item it{L, parts, B, delta, ld_d, y_prev, ld_y, phantoms, received, grad, upd};
+  ppx_wgrad_item it{L, parts, B, delta, ld_d, y_prev, ld_y, phantoms, received, grad, upd, 1};
   return ppx_wgrad(ctx, dt, 1, &it, stream);
 }
 

@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import torch
 
@@ -95,6 +96,9 @@ class PhantomEngine:
                 self.Y[1][jj][l] = self.Y[0][jj][l]
         self.Tgt = [[torch.empty((B, s), dtype=dtype, device=self.dev) for _ in range(R)] for _ in range(2)]
         self.D = [[torch.empty((B, s), dtype=dtype, device=self.dev) for _ in range(2)] for _ in range(R)]
+        # phantom all-gather buffers; on multi-GPU runs the batch is split in two halves
+        # [2][p][B/2, ldk] so each half's all-gather hides behind the other half's GEMMs
+        self.halves = 2 if (world > 1 and B % 128 == 0 and os.environ.get("PPX_HALVES", "1") == "2") else 1
         self.G = [torch.zeros((p, B, ldk), dtype=dtype, device=self.dev) for _ in range(L)]
         self.H = [torch.zeros((p, B, ldk), dtype=dtype, device=self.dev) for _ in range(L)]
         self.loss = torch.zeros(1, dtype=f32, device=self.dev)
@@ -219,27 +223,51 @@ class PhantomEngine:
         self._keep.append(arr)
         return arr
 
+    def _gh(self, l, h):
+        """Phantom buffer of batch half h of layer l ([p, B/H, ldk] at offset h)."""
+        Bh = self.B // self.halves
+        return self.G[l].data_ptr() + h * self.p * Bh * self.off["ldk"] * self.G[l].element_size()
+
     def _forward(self, par, S, train=True):
-        st, pdt, B, s, R = S.cuda_stream, self.pdt, self.B, self.s, self.R
-        slot = B * self.off["ldk"]
-        for l in range(self.L):
-            ios = [self._io(jj, l, par, x=self.Y[par][jj][l].data_ptr(), ld_x=s) for jj in range(R)]
-            self._call("ppx_compress_n", pdt, R, self._ios(ios), B, self.G[l].data_ptr(), st)
+        st, pdt, B, s, R, H = S.cuda_stream, self.pdt, self.B, self.s, self.R, self.halves
+        Bh = B // H
+        esz = self.Y[par][0][0].element_size()
+        rows = lambda t, h: t.data_ptr() + h * Bh * s * esz   # noqa: E731  (row block h of a [B, s] buffer)
+        mean = self.reduction == "mean"
+        ag_done = {}
+
+        def compress(l, h):
+            ios = [self._io(jj, l, par, x=rows(self.Y[par][jj][l], h), ld_x=s) for jj in range(R)]
+            self._call("ppx_compress_n", pdt, R, self._ios(ios), Bh, self._gh(l, h), st)
             if self.world > 1:
                 self._join(S, self.comm_stream)
-                self._call("ppx_all_gather", pdt, self.G[l].data_ptr(), slot, R, self.comm_stream.cuda_stream)
-                self._join(self.comm_stream, S)
+                self._call("ppx_all_gather", pdt, self._gh(l, h), Bh * self.off["ldk"], R,
+                           self.comm_stream.cuda_stream)
+                ev = torch.cuda.Event()
+                ev.record(self.comm_stream)
+                ag_done[(l, h)] = ev
+
+        # software pipeline over batch halves: the all-gather of one half overlaps the other
+        # half's GEMMs (H = 2 on multi-GPU runs; H = 1 has nothing to hide)
+        for h in range(H):
+            compress(0, h)
+        for l in range(self.L):
             last = train and l == self.L - 1
-            ios = []
-            for jj in range(R):
-                kw = dict(x=self.Y[par][jj][l].data_ptr(), ld_x=s, out=self.Y[par][jj][l + 1].data_ptr(), ld_out=s)
-                if last:
-                    kw.update(aux=self.D[jj][0].data_ptr(), ld_aux=s, target=self.Tgt[par][jj].data_ptr(), ld_t=s,
-                              colsum=self.gbias[jj, l].data_ptr())
-                ios.append(self._io(jj, l, par, **kw))
-            mean = self.reduction == "mean"
-            self._call("ppx_forward_n", pdt, R, self._ios(ios), B, self.act.code, self.G[l].data_ptr(), int(last),
-                       1.0 / B if mean else 1.0, 0.5 / B if mean else 0.5, self.loss.data_ptr() if last else None, st)
+            for h in range(H):
+                if (l, h) in ag_done:
+                    S.wait_event(ag_done[(l, h)])
+                ios = []
+                for jj in range(R):
+                    kw = dict(x=rows(self.Y[par][jj][l], h), ld_x=s, out=rows(self.Y[par][jj][l + 1], h), ld_out=s)
+                    if last:
+                        kw.update(aux=rows(self.D[jj][0], h), ld_aux=s, target=rows(self.Tgt[par][jj], h), ld_t=s,
+                                  colsum=self.gbias[jj, l].data_ptr())
+                    ios.append(self._io(jj, l, par, **kw))
+                self._call("ppx_forward_n", pdt, R, self._ios(ios), Bh, self.act.code, self._gh(l, h), int(last),
+                           1.0 / B if mean else 1.0, 0.5 / B if mean else 0.5,
+                           self.loss.data_ptr() if last else None, st)
+                if l + 1 < self.L:
+                    compress(l + 1, h)
 
     def _launch_wgrad(self, items, st):
         arr = (_lib.WgradItem * len(items))(*items)
@@ -266,7 +294,8 @@ class PhantomEngine:
                 j = self.local[jj]
                 items = [_lib.WgradItem(ctypes.pointer(self._layer(jj, l, par)), _lib.GRAD_LOCAL | _lib.GRAD_DEC, B,
                                         self.D[jj][cur].data_ptr(), s, self.Y[par][jj][l].data_ptr(), s,
-                                        self.G[l].data_ptr(), None, None, ctypes.pointer(self._update(jj, l, par)))]
+                                        self.G[l].data_ptr(), None, None, ctypes.pointer(self._update(jj, l, par)),
+                                        self.halves)]
                 if l < L - 1:   # d compressor of layer l+1 (its r arrived one layer ago)
                     items.append(_lib.WgradItem(ctypes.pointer(self._layer(jj, l + 1, par)), _lib.GRAD_COMP, B,
                                                 self.D[jj][cur].data_ptr(), s, self.Y[par][jj][l + 1].data_ptr(), s,
