@@ -12,6 +12,7 @@ namespace ppx {
 struct GemmParams;
 template <bool kTF32>
 cudaError_t launch_gemm(const GemmParams& P, int grid, cudaStream_t st);
+cudaError_t launch_gemm_pair(const GemmParams& P, int grid, cudaStream_t st);
 
 __device__ __forceinline__ float ld_elem(const void* p, int64_t i, bool f32) {
   return f32 ? reinterpret_cast<const float*>(p)[i] : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);

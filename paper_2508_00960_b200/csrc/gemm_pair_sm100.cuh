@@ -1,0 +1,206 @@
+// 2-SM (cta_group::2) variant of the grouped GEMM for the bf16 tier.
+//
+// A CTA pair (cluster of 2) owns a 256 x BN output tile: each CTA stages 128 rows of A and BN/2
+// rows of B; the leader issues M=256 tcgen05.mma into both CTAs' TMEM.  A stage carries
+// K = 128 (two 64-wide SWIZZLE_128B atoms), so one stage is 8 MMAs = 1024 tensor cycles per SM
+// between barrier round trips (the 1-SM kernel's 4 MMAs / 512 cycles leaves the tensor pipe
+// ~25% idle on barrier/issue latency).  Double-buffered TMEM accumulators (2 x 256 columns) keep
+// the epilogue of tile i under the MMAs of tile i+1.  Problems, segments, slot-blocked K / N
+// coordinates and the epilogue are shared with gemm_sm100.cuh (same GemmParams).
+#pragma once
+#include "gemm_sm100.cuh"
+
+namespace ppx {
+
+constexpr int PBK = 128;                         // K elements per stage (2 atoms)
+constexpr int PSTAGES = 3;
+constexpr int PA_STAGE = BM * 2 * ROW_BYTES;     // 32 KB: [2 K-atoms][128 rows][128 B]
+constexpr int PB_STAGE = 128 * 2 * ROW_BYTES;    // 32 KB: [2 K-atoms][<=128 rows][128 B]
+constexpr int PSMEM_BYTES = PSTAGES * (PA_STAGE + PB_STAGE) + 1024 + 256;
+
+__device__ __forceinline__ void tma4_pair(const CUtensorMap* map, uint32_t bar, uint32_t dst, int c0, int c1, int c2,
+                                          int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5, %6}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma5_pair(const CUtensorMap* map, uint32_t bar, uint32_t dst, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %3, "
+      "%4, %5, %6}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(0), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+// Operand maps for this kernel (host side, ppx.cu):
+//   K-major:          4D {64, rows, K/64 atoms, slots}  box {64, rows_per_cta, 2, 1}  -> [katom][rows][128B]
+//   MN-major (mode1): 4D {64, K rows, MN atoms, slots}  box {64, 128, natoms, 1}     -> [atom][128 K rows][128B]
+//   MN-major (mode2): 5D {64, 8, MN atoms, K/8, slots}  box {64, 8, natoms, 16, 1}   -> [kgroup][atom][8][128B]
+__global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_constant__ GemmParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t sA = base_u32;
+  const uint32_t sB = sA + PSTAGES * PA_STAGE;
+  const uint32_t sBar = sB + PSTAGES * PB_STAGE;
+  auto full_bar = [&](int s) { return sBar + 8u * s; };
+  auto empty_bar = [&](int s) { return sBar + 8u * (PSTAGES + s); };
+  auto tfull_bar = [&](int s) { return sBar + 8u * (2 * PSTAGES + s); };
+  auto tempty_bar = [&](int s) { return sBar + 8u * (2 * PSTAGES + 2 + s); };
+  const uint32_t tmem_slot = sBar + 8u * (2 * PSTAGES + 4);
+  uint8_t* smem_gen = smem_raw + (base_u32 - smem_u32(smem_raw));
+  volatile uint32_t* tmem_slot_ptr = reinterpret_cast<volatile uint32_t*>(smem_gen + (tmem_slot - base_u32));
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+  constexpr int CHA = 64;       // bf16 elements per 128-byte atom
+  constexpr int KMMA = 16;      // K per tcgen05.mma (bf16)
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < P.nmaps; ++i) prefetch_map(&P.maps[i]);
+    for (int s = 0; s < PSTAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(tfull_bar(s), 1);
+      mbar_init(tempty_bar(s), 8);   // 4 epilogue warps in each CTA of the pair
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot_ptr;
+
+  const int total = P.total_tiles;
+  const int t0 = (int)(blockIdx.x >> 1);
+  const int tstep = (int)(gridDim.x >> 1);
+
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs) =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = t0; t < total; t += tstep) {
+        TileCoord tc = tile_coord<2 * BM>(P, t);
+        const Problem& pr = P.probs[tc.prob];
+        const int bnc = pr.BN / 2;
+        const uint32_t bytes = (uint32_t)(BM + bnc) * 2u * ROW_BYTES * 2u;   // both CTAs, 2 K-atoms each
+        const int am0 = tc.m0 + (int)crank * BM;
+        const int bn0 = tc.nin + (int)crank * bnc;
+        for (int sg = 0; sg < pr.nsegs; ++sg) {
+          const Segment& seg = pr.segs[sg];
+          const CUtensorMap* ma = &P.maps[seg.a.map];
+          const CUtensorMap* mb = &P.maps[seg.b.map];
+          for (int kt = 0; kt < seg.k_tiles; ++kt) {
+            const int kblk = kt / seg.kpb;
+            const int kin = (kt - kblk * seg.kpb) * PBK;
+            mbar_wait(empty_bar(stage), phase ^ 1u);
+            if (leader) mbar_expect_tx(full_bar(stage), bytes);
+            const uint32_t fb = mapa_shared(full_bar(stage), 0);
+            const uint32_t da = sA + stage * PA_STAGE;
+            const uint32_t db = sB + stage * PB_STAGE;
+            const int slot_a = op_slot(seg.a, kblk, tc.qn);
+            const int slot_b = op_slot(seg.b, kblk, tc.qn);
+            if (!seg.a.mn) tma4_pair(ma, fb, da, 0, am0, kin / CHA, slot_a);
+            else if (seg.a.atoms4d == 2) tma5_pair(ma, fb, da, am0 / CHA, kin / 8, slot_a);
+            else tma4_pair(ma, fb, da, 0, kin, am0 / CHA, slot_a);
+            if (!seg.b.mn) tma4_pair(mb, fb, db, 0, bn0, kin / CHA, slot_b);
+            else if (seg.b.atoms4d == 2) tma5_pair(mb, fb, db, bn0 / CHA, kin / 8, slot_b);
+            else tma4_pair(mb, fb, db, 0, kin, bn0 / CHA, slot_b);
+            if (++stage == PSTAGES) { stage = 0; phase ^= 1u; }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA, one lane) =====================
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int iter = 0;
+      for (int t = t0; t < total; t += tstep, ++iter) {
+        TileCoord tc = tile_coord<2 * BM>(P, t);
+        const Problem& pr = P.probs[tc.prob];
+        const int as = iter & 1;
+        const uint32_t aphase = (iter >> 1) & 1;
+        mbar_wait(tempty_bar(as), aphase ^ 1u);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + as * BN_MAX;
+        const int bnc = pr.BN / 2;
+        uint32_t accum = 0;
+        for (int sg = 0; sg < pr.nsegs; ++sg) {
+          const Segment& seg = pr.segs[sg];
+          const uint32_t idesc = seg.idesc;
+          // per-operand descriptor geometry (bytes): LBO, SBO, advance per MMA, advance per K atom
+          uint32_t a_lbo, a_sbo, a_step, a_katom, b_lbo, b_sbo, b_step, b_katom;
+          if (!seg.a.mn) { a_lbo = 16; a_sbo = 1024; a_step = 32; a_katom = BM * ROW_BYTES; }
+          else if (seg.a.atoms4d == 2) {
+            a_lbo = 1024; a_sbo = (BM / CHA) * 1024; a_step = 2 * a_sbo; a_katom = 4 * a_step;
+          } else { a_lbo = PBK * ROW_BYTES; a_sbo = 1024; a_step = KMMA * ROW_BYTES; a_katom = 4 * a_step; }
+          if (!seg.b.mn) { b_lbo = 16; b_sbo = 1024; b_step = 32; b_katom = bnc * ROW_BYTES; }
+          else if (seg.b.atoms4d == 2) {
+            b_lbo = 1024; b_sbo = (bnc / CHA) * 1024; b_step = 2 * b_sbo; b_katom = 4 * b_step;
+          } else { b_lbo = PBK * ROW_BYTES; b_sbo = 1024; b_step = KMMA * ROW_BYTES; b_katom = 4 * b_step; }
+          for (int kt = 0; kt < seg.k_tiles; ++kt) {
+            mbar_wait(full_bar(stage), phase);
+            tc_fence_after();
+            const uint32_t da = sA + stage * PA_STAGE;
+            const uint32_t db = sB + stage * PB_STAGE;
+#pragma unroll
+            for (int ka = 0; ka < 2; ++ka) {
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                const uint64_t ad = sdesc(da + ka * a_katom + kk * a_step, a_lbo, a_sbo);
+                const uint64_t bd = sdesc(db + ka * b_katom + kk * b_step, b_lbo, b_sbo);
+                mma_pair(tmem_d, ad, bd, idesc, accum);
+                accum = 1;
+              }
+            }
+            commit_pair(empty_bar(stage));
+            if (++stage == PSTAGES) { stage = 0; phase ^= 1u; }
+          }
+        }
+        commit_pair(tfull_bar(as));
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    epilogue_loop<2 * BM, true>(P, tmem_base, tfull_bar(0), tempty_bar(0), t0, tstep, crank, warp, lane);
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+}  // namespace ppx

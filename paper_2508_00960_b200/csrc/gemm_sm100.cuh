@@ -114,6 +114,7 @@ struct alignas(64) GemmParams {
   int nmaps;
   int nprobs;
   int total_tiles;
+  int dbg;             // debug: bit0 = skip the epilogue body (TMEM drain only by arrival)
 };
 
 // ------------------------------------------------------------------------------------------
@@ -197,6 +198,20 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   d |= static_cast<uint64_t>(1) << 46;
   d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
   return d;
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
 template <bool kTF32>
@@ -324,6 +339,7 @@ struct TileCoord {
   int prob, m0, qn, nin;
 };
 
+template <int MT>
 __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, int t) {
   int pi = 0;
 #pragma unroll 1
@@ -335,7 +351,7 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, int t) {
   int nt = local - mt * ntn;
   TileCoord c;
   c.prob = pi;
-  c.m0 = mt * BM;
+  c.m0 = mt * MT;
   c.qn = nt / pr.npb;
   c.nin = (nt - c.qn * pr.npb) * pr.BN;
   return c;
@@ -346,164 +362,33 @@ __device__ __forceinline__ int op_slot(const Operand& o, int kblk, int qn) {
   return o.slot_base + raw + (raw >= o.slot_skip ? 1 : 0);
 }
 
-template <bool kTF32>
-__global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmParams P) {
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
-  const uint32_t sA = base_u32;
-  const uint32_t sB = sA + STAGES * A_STAGE_BYTES;
-  const uint32_t sBar = sB + STAGES * B_STAGE_BYTES;
-  // barrier layout: full[STAGES], empty[STAGES], tfull[2], tempty[2], tmem addr slot
-  auto full_bar = [&](int s) { return sBar + 8u * s; };
-  auto empty_bar = [&](int s) { return sBar + 8u * (STAGES + s); };
-  auto tfull_bar = [&](int s) { return sBar + 8u * (2 * STAGES + s); };
-  auto tempty_bar = [&](int s) { return sBar + 8u * (2 * STAGES + 2 + s); };
-  const uint32_t tmem_slot = sBar + 8u * (2 * STAGES + 4);
-  uint8_t* smem_gen = smem_raw + (base_u32 - smem_u32(smem_raw));
-  volatile uint32_t* tmem_slot_ptr =
-      reinterpret_cast<volatile uint32_t*>(smem_gen + (tmem_slot - base_u32));
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  constexpr int ESIZE = kTF32 ? 4 : 2;
-  constexpr int BK = ROW_BYTES / ESIZE;     // elements of K per stage
-  constexpr int CH = ROW_BYTES / ESIZE;     // MN-major atom width in elements
-  constexpr int KMMA = 32 / ESIZE;          // K per tcgen05.mma
-  constexpr int NK = BK / KMMA;             // MMAs per stage (4)
-
-  if (warp == 0 && lane == 0) {
-    for (int i = 0; i < P.nmaps; ++i) prefetch_map(&P.maps[i]);
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full_bar(s), 1);
-      mbar_init(empty_bar(s), 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(tfull_bar(s), 1);
-      mbar_init(tempty_bar(s), 4);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot_ptr;
-
+// ------------------------------------------------------------------------------------------
+// epilogue warps (4 warps = the 4 TMEM lane quadrants): drain one accumulator stage per tile
+// ------------------------------------------------------------------------------------------
+template <int MT, bool kPair>
+__device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem_base, uint32_t tfull0,
+                                              uint32_t tempty0, int t0, int tstep, uint32_t crank, int warp,
+                                              int lane) {
   const int total = P.total_tiles;
-
-  if (warp == 0) {
-    // ===================== TMA producer =====================
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        TileCoord tc = tile_coord(P, t);
-        const Problem& pr = P.probs[tc.prob];
-        const uint32_t bytes = (uint32_t)(BM + pr.BN) * ROW_BYTES;
-        for (int sg = 0; sg < pr.nsegs; ++sg) {
-          const Segment& seg = pr.segs[sg];
-          const CUtensorMap* ma = &P.maps[seg.a.map];
-          const CUtensorMap* mb = &P.maps[seg.b.map];
-          for (int kt = 0; kt < seg.k_tiles; ++kt) {
-            const int kblk = kt / seg.kpb;
-            const int kin = (kt - kblk * seg.kpb) * BK;
-            mbar_wait(empty_bar(stage), phase ^ 1u);
-            mbar_expect_tx(full_bar(stage), bytes);
-            const uint32_t da = sA + stage * A_STAGE_BYTES;
-            const uint32_t db = sB + stage * B_STAGE_BYTES;
-            const int slot_a = op_slot(seg.a, kblk, tc.qn);
-            const int slot_b = op_slot(seg.b, kblk, tc.qn);
-            if (!seg.a.mn) {
-              tma_load_3d(ma, full_bar(stage), da, kin, tc.m0, slot_a);
-            } else if (seg.a.atoms4d == 2) {
-              tma_load_5d(ma, full_bar(stage), da, tc.m0 / CH, kin / 8, slot_a);
-            } else if (seg.a.atoms4d) {
-              tma_load_4d(ma, full_bar(stage), da, 0, kin, tc.m0 / CH, slot_a);
-            } else {
-#pragma unroll 1
-              for (int c = 0; c < BM / CH; ++c)
-                tma_load_3d(ma, full_bar(stage), da + c * (BK * ROW_BYTES), tc.m0 + c * CH, kin, slot_a);
-            }
-            if (!seg.b.mn) {
-              tma_load_3d(mb, full_bar(stage), db, kin, tc.nin, slot_b);
-            } else if (seg.b.atoms4d) {
-              tma_load_4d(mb, full_bar(stage), db, 0, kin, tc.nin / CH, slot_b);
-            } else {
-#pragma unroll 1
-              for (int c = 0; c < pr.BN / CH; ++c)
-                tma_load_3d(mb, full_bar(stage), db + c * (BK * ROW_BYTES), tc.nin + c * CH, kin, slot_b);
-            }
-            if (++stage == STAGES) { stage = 0; phase ^= 1u; }
-          }
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int iter = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++iter) {
-        TileCoord tc = tile_coord(P, t);
-        const Problem& pr = P.probs[tc.prob];
-        const int as = iter & 1;
-        const uint32_t aphase = (iter >> 1) & 1;
-        mbar_wait(tempty_bar(as), aphase ^ 1u);
-        tc_fence_after();
-        const uint32_t tmem_d = tmem_base + as * BN_MAX;
-        uint32_t accum = 0;
-        for (int sg = 0; sg < pr.nsegs; ++sg) {
-          const Segment& seg = pr.segs[sg];
-          for (int kt = 0; kt < seg.k_tiles; ++kt) {
-            mbar_wait(full_bar(stage), phase);
-            tc_fence_after();
-            const uint32_t da = sA + stage * A_STAGE_BYTES;
-            const uint32_t db = sB + stage * B_STAGE_BYTES;
-#pragma unroll
-            for (int kk = 0; kk < NK; ++kk) {
-              // MN-major A: atom-major tile (LBO = atom stride, SBO = 1024) or the interleaved
-              // canonical tile (LBO = 1024 between MN atoms, SBO = 2 KB between 8-row K groups)
-              uint64_t ad = !seg.a.mn ? sdesc(da + kk * 32, 16, 1024)
-                            : (seg.a.atoms4d == 2 ? sdesc(da + kk * (KMMA / 8) * (BM / CH) * 1024, 1024, (BM / CH) * 1024)
-                                                  : sdesc(da + kk * (KMMA * ROW_BYTES), BK * ROW_BYTES, 1024));
-              uint64_t bd = seg.b.mn ? sdesc(db + kk * (KMMA * ROW_BYTES), BK * ROW_BYTES, 1024)
-                                     : sdesc(db + kk * 32, 16, 1024);
-              mma_issue<kTF32>(tmem_d, ad, bd, seg.idesc, accum);
-              accum = 1;
-            }
-            mma_commit(empty_bar(stage));
-            if (++stage == STAGES) { stage = 0; phase ^= 1u; }
-          }
-        }
-        mma_commit(tfull_bar(as));
-      }
-    }
-    __syncwarp();
-  } else if (warp >= 4) {
-    // ===================== epilogue =====================
+  auto tfull_bar = [&](int s) { return tfull0 + 8u * s; };
+  auto tempty_bar = [&](int s) { return tempty0 + 8u * s; };
     const int wq = warp - 4;  // TMEM lane quadrant
     int iter = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++iter) {
-      TileCoord tc = tile_coord(P, t);
+    for (int t = t0; t < total; t += tstep, ++iter) {
+      TileCoord tc = tile_coord<MT>(P, t);
       const Problem& pr = P.probs[tc.prob];
       const Epilogue& E = pr.epi;
       const int as = iter & 1;
       const uint32_t aphase = (iter >> 1) & 1;
       mbar_wait(tfull_bar(as), aphase);
       tc_fence_after();
-      const int row = tc.m0 + wq * 32 + lane;
+      const int row = tc.m0 + (int)crank * BM + wq * 32 + lane;
       const bool row_ok = row < pr.M;
       const int oslot = tc.qn + (tc.qn >= E.out_skip ? 1 : 0);
       const uint32_t flags = E.flags;
       float loss_acc = 0.f;
       bool bad = false;
-      const int nchunks = (pr.BN + 31) / 32;
+      const int nchunks = (P.dbg & 1) ? 0 : (pr.BN + 31) / 32;
       for (int c = 0; c < nchunks; ++c) {
         float v[32];
         tmem_ld32(tmem_base + as * BN_MAX + c * 32 + ((uint32_t)(wq * 32) << 16), v);
@@ -614,8 +499,154 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
       if ((flags & EP_FINITE) && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(E.bad, 1);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty_bar(as));
+      if (lane == 0) {
+        if constexpr (kPair) mbar_arrive_cluster(mapa_shared(tempty_bar(as), 0));
+        else mbar_arrive(tempty_bar(as));
+      }
     }
+}
+
+template <bool kTF32>
+__global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t sA = base_u32;
+  const uint32_t sB = sA + STAGES * A_STAGE_BYTES;
+  const uint32_t sBar = sB + STAGES * B_STAGE_BYTES;
+  // barrier layout: full[STAGES], empty[STAGES], tfull[2], tempty[2], tmem addr slot
+  auto full_bar = [&](int s) { return sBar + 8u * s; };
+  auto empty_bar = [&](int s) { return sBar + 8u * (STAGES + s); };
+  auto tfull_bar = [&](int s) { return sBar + 8u * (2 * STAGES + s); };
+  auto tempty_bar = [&](int s) { return sBar + 8u * (2 * STAGES + 2 + s); };
+  const uint32_t tmem_slot = sBar + 8u * (2 * STAGES + 4);
+  uint8_t* smem_gen = smem_raw + (base_u32 - smem_u32(smem_raw));
+  volatile uint32_t* tmem_slot_ptr =
+      reinterpret_cast<volatile uint32_t*>(smem_gen + (tmem_slot - base_u32));
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  constexpr int ESIZE = kTF32 ? 4 : 2;
+  constexpr int BK = ROW_BYTES / ESIZE;     // elements of K per stage
+  constexpr int CH = ROW_BYTES / ESIZE;     // MN-major atom width in elements
+  constexpr int KMMA = 32 / ESIZE;          // K per tcgen05.mma
+  constexpr int NK = BK / KMMA;             // MMAs per stage (4)
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < P.nmaps; ++i) prefetch_map(&P.maps[i]);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(tfull_bar(s), 1);
+      mbar_init(tempty_bar(s), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot_ptr;
+
+  const int total = P.total_tiles;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        TileCoord tc = tile_coord<BM>(P, t);
+        const Problem& pr = P.probs[tc.prob];
+        const uint32_t bytes = (uint32_t)(BM + pr.BN) * ROW_BYTES;
+        for (int sg = 0; sg < pr.nsegs; ++sg) {
+          const Segment& seg = pr.segs[sg];
+          const CUtensorMap* ma = &P.maps[seg.a.map];
+          const CUtensorMap* mb = &P.maps[seg.b.map];
+          for (int kt = 0; kt < seg.k_tiles; ++kt) {
+            const int kblk = kt / seg.kpb;
+            const int kin = (kt - kblk * seg.kpb) * BK;
+            mbar_wait(empty_bar(stage), phase ^ 1u);
+            mbar_expect_tx(full_bar(stage), bytes);
+            const uint32_t da = sA + stage * A_STAGE_BYTES;
+            const uint32_t db = sB + stage * B_STAGE_BYTES;
+            const int slot_a = op_slot(seg.a, kblk, tc.qn);
+            const int slot_b = op_slot(seg.b, kblk, tc.qn);
+            if (!seg.a.mn) {
+              tma_load_3d(ma, full_bar(stage), da, kin, tc.m0, slot_a);
+            } else if (seg.a.atoms4d == 2) {
+              tma_load_5d(ma, full_bar(stage), da, tc.m0 / CH, kin / 8, slot_a);
+            } else if (seg.a.atoms4d) {
+              tma_load_4d(ma, full_bar(stage), da, 0, kin, tc.m0 / CH, slot_a);
+            } else {
+#pragma unroll 1
+              for (int c = 0; c < BM / CH; ++c)
+                tma_load_3d(ma, full_bar(stage), da + c * (BK * ROW_BYTES), tc.m0 + c * CH, kin, slot_a);
+            }
+            if (!seg.b.mn) {
+              tma_load_3d(mb, full_bar(stage), db, kin, tc.nin, slot_b);
+            } else if (seg.b.atoms4d) {
+              tma_load_4d(mb, full_bar(stage), db, 0, kin, tc.nin / CH, slot_b);
+            } else {
+#pragma unroll 1
+              for (int c = 0; c < pr.BN / CH; ++c)
+                tma_load_3d(mb, full_bar(stage), db + c * (BK * ROW_BYTES), tc.nin + c * CH, kin, slot_b);
+            }
+            if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int iter = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++iter) {
+        TileCoord tc = tile_coord<BM>(P, t);
+        const Problem& pr = P.probs[tc.prob];
+        const int as = iter & 1;
+        const uint32_t aphase = (iter >> 1) & 1;
+        mbar_wait(tempty_bar(as), aphase ^ 1u);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + as * BN_MAX;
+        uint32_t accum = 0;
+        for (int sg = 0; sg < pr.nsegs; ++sg) {
+          const Segment& seg = pr.segs[sg];
+          for (int kt = 0; kt < seg.k_tiles; ++kt) {
+            if (!(P.dbg & 2)) mbar_wait(full_bar(stage), phase);
+            tc_fence_after();
+            const uint32_t da = sA + stage * A_STAGE_BYTES;
+            const uint32_t db = sB + stage * B_STAGE_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < NK; ++kk) {
+              // MN-major A: atom-major tile (LBO = atom stride, SBO = 1024) or the interleaved
+              // canonical tile (LBO = 1024 between MN atoms, SBO = 2 KB between 8-row K groups)
+              uint64_t ad = !seg.a.mn ? sdesc(da + kk * 32, 16, 1024)
+                            : (seg.a.atoms4d == 2 ? sdesc(da + kk * (KMMA / 8) * (BM / CH) * 1024, 1024, (BM / CH) * 1024)
+                                                  : sdesc(da + kk * (KMMA * ROW_BYTES), BK * ROW_BYTES, 1024));
+              uint64_t bd = seg.b.mn ? sdesc(db + kk * (KMMA * ROW_BYTES), BK * ROW_BYTES, 1024)
+                                     : sdesc(db + kk * 32, 16, 1024);
+              mma_issue<kTF32>(tmem_d, ad, bd, seg.idesc, accum);
+              accum = 1;
+            }
+            mma_commit(empty_bar(stage));
+            if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+          }
+        }
+        mma_commit(tfull_bar(as));
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    epilogue_loop<BM, false>(P, tmem_base, tfull_bar(0), tempty_bar(0), blockIdx.x, gridDim.x, 0u, warp, lane);
   }
 
   tc_fence_before();

@@ -22,6 +22,7 @@
 #include "../../include/ppx.h"
 #include "elementwise.cuh"
 #include "gemm_sm100.cuh"
+#include "gemm_pair_sm100.cuh"
 
 struct ppx_ctx {
   int world = 1, rank = 0, device = 0, num_sms = 148;
@@ -158,11 +159,15 @@ struct Builder {
   }
 
   bool use4d = getenv("PPX_NO_4D") == nullptr;
+  // 2-SM (cta_group::2) kernel for bf16 launches whose operands tile into 64-wide atoms
+  bool want_pair = false, use_pair = false;
+  int BKf = 64;   // K per stage of the kernel actually launched
   // MN-major A (activations / deltas of the weight-gradient GEMMs) as the interleaved 5D tile
   bool use5d = getenv("PPX_NO_5D") == nullptr;
 
   Builder(ppx_ctx* c, ppx_dtype dt, void* stream) : ctx(c), st((cudaStream_t)stream), tf32(dt == PPX_FP32) {
     esize = tf32 ? 4 : 2;
+    want_pair = !tf32 && getenv("PPX_NO_PAIR") == nullptr;
     BK = ppx::ROW_BYTES / esize;
     CH = BK;
     memset(&P, 0, sizeof(P));
@@ -216,6 +221,85 @@ struct Builder {
     }
     map_cache[key] = P.nmaps;
     return P.nmaps++;
+  }
+
+  int add_map_nd(const View& v, int rank, const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                 int tag) {
+    if (!ok()) return -1;
+    MapKey key{v.ptr, v.cols, v.rows, v.slots, v.ld, v.slot_stride, tag, (int)(box[1] * 1000 + box[2])};
+    auto hit = map_cache.find(key);
+    if (hit != map_cache.end()) return hit->second;
+    if (P.nmaps >= ppx::MAX_MAPS) { error(PPX_E_CONFIG, "too many tensor maps in one launch"); return -1; }
+    if (!get_encode()) { error(PPX_E_CUDA, "cuTensorMapEncodeTiled unavailable"); return -1; }
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = g_encode(&P.maps[P.nmaps], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(v.ptr), dims,
+                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { error(PPX_E_CUDA, "cuTensorMapEncodeTiled failed (2-SM operand map)"); return -1; }
+    map_cache[key] = P.nmaps;
+    return P.nmaps++;
+  }
+
+  // 2-SM kernel operand map (gemm_pair_sm100.cuh): K-major -> [2 K-atoms][rows][128 B] per stage,
+  // MN-major -> interleaved [16 K groups][atoms][8][128 B] (5D) or [atoms][128 K rows][128 B] (4D)
+  int pair_map(const View& v, bool mn, int rows_or_atoms, bool interleaved, int& mode) {
+    const cuuint64_t es = 2;
+    if (!mn) {
+      cuuint64_t dims[4] = {64, (cuuint64_t)v.rows, (cuuint64_t)(v.cols / 64), (cuuint64_t)v.slots};
+      cuuint64_t strides[3] = {(cuuint64_t)v.ld * es, 128, (cuuint64_t)v.slot_stride * es};
+      cuuint32_t box[4] = {64, (cuuint32_t)rows_or_atoms, 2, 1};
+      mode = 0;
+      return add_map_nd(v, 4, dims, strides, box, -100);
+    }
+    if (interleaved) {
+      cuuint64_t dims[5] = {64, 8, (cuuint64_t)(v.cols / 64), (cuuint64_t)(v.rows / 8), (cuuint64_t)v.slots};
+      cuuint64_t strides[4] = {(cuuint64_t)v.ld * es, 128, (cuuint64_t)(8 * v.ld) * es, (cuuint64_t)v.slot_stride * es};
+      cuuint32_t box[5] = {64, 8, (cuuint32_t)rows_or_atoms, 16, 1};
+      mode = 2;
+      return add_map_nd(v, 5, dims, strides, box, -101);
+    }
+    cuuint64_t dims[4] = {64, (cuuint64_t)v.rows, (cuuint64_t)(v.cols / 64), (cuuint64_t)v.slots};
+    cuuint64_t strides[3] = {(cuuint64_t)v.ld * es, 128, (cuuint64_t)v.slot_stride * es};
+    cuuint32_t box[4] = {64, 128, (cuuint32_t)rows_or_atoms, 1};
+    mode = 1;
+    return add_map_nd(v, 4, dims, strides, box, -102);
+  }
+
+  void finalize_pair(Problem* pr, const Opnd& a, const Opnd& b, int k_tiles, int kpb) {
+    if (pr->nsegs >= ppx::MAX_SEGS) { error(PPX_E_CONFIG, "too many K segments"); return; }
+    Segment& s = pr->segs[pr->nsegs++];
+    const int bnc = pr->BN / 2;
+    int ma = 0, mb = 0;
+    const int ia = pair_map(a.v, a.mn, a.mn ? ppx::BM / 64 : ppx::BM, a.mn && a.v.rows % 8 == 0 && use5d, ma);
+    const int ib = pair_map(b.v, b.mn, b.mn ? bnc / 64 : bnc, false, mb);
+    if (!ok()) return;
+    s.a.map = (int8_t)ia;
+    s.a.mn = (int8_t)a.mn;
+    s.a.atoms4d = (int8_t)ma;
+    s.a.slot_src = (int8_t)a.slot_src;
+    s.a.slot_base = a.slot_base;
+    s.a.slot_skip = a.slot_skip;
+    s.b.map = (int8_t)ib;
+    s.b.mn = (int8_t)b.mn;
+    s.b.atoms4d = (int8_t)mb;
+    s.b.slot_src = (int8_t)b.slot_src;
+    s.b.slot_base = b.slot_base;
+    s.b.slot_skip = b.slot_skip;
+    s.k_tiles = k_tiles;
+    s.kpb = kpb;
+    uint32_t d = make_idesc(false, a.mn, b.mn, pr->BN);
+    d = (d & ~(0x1Fu << 24)) | ((uint32_t)(2 * ppx::BM) >> 4) << 24;   // M = 256 (cta_group::2)
+    s.idesc = d;
+  }
+
+  // every operand must tile into whole 64-wide atoms for the 2-SM kernel
+  bool pair_shapes_ok() const {
+    for (int i = 0; i < P.nprobs; ++i)
+      for (const PendingSeg& ps : pend[i]) {
+        if (ps.a.v.cols % 64 || ps.b.v.cols % 64) return false;
+        if (ps.a.mn && ps.a.v.rows % 8) return false;
+      }
+    return true;
   }
 
   // MN-major operand as ONE 4D box per stage: {CH elements, BK rows, atoms, 1} over the view
@@ -303,7 +387,8 @@ struct Builder {
 
   struct PendingSeg {
     Opnd a, b;
-    int k_tiles, kpb;
+    int kext;    // K elements per block (rounded up to BK)
+    int nkblk;   // number of K blocks (slots walked by a K-blocked segment; 1 otherwise)
   };
   std::vector<PendingSeg> pend[ppx::MAX_PROBS];
   bool prob_bmn[ppx::MAX_PROBS] = {};
@@ -334,15 +419,19 @@ struct Builder {
   }
 
   // record a K segment; tensor maps are built in launch() once every problem's BN is final
+  // callers pass k_tiles / kpb in units of BK; they are kept as (K extent per block, blocks) so
+  // launch() can re-tile K for the 2-SM kernel's 128-wide stages
   void add_segment(Problem* pr, Opnd a, Opnd b, int k_tiles, int kpb) {
     if (!ok() || !pr) return;
-    if (k_tiles <= 0) { error(PPX_E_CONFIG, "empty K segment"); return; }
-    pend[pr - P.probs].push_back({a, b, k_tiles, kpb});
+    if (k_tiles <= 0 || kpb <= 0 || k_tiles % kpb) { error(PPX_E_CONFIG, "empty or ragged K segment"); return; }
+    pend[pr - P.probs].push_back({a, b, kpb * BK, k_tiles / kpb});
   }
 
   void finalize(Problem* pr, const PendingSeg& ps) {
     Opnd a = ps.a, b = ps.b;
-    const int k_tiles = ps.k_tiles, kpb = ps.kpb;
+    const int kpb = (int)cdiv(ps.kext, BKf);
+    const int k_tiles = kpb * ps.nkblk;
+    if (use_pair) { finalize_pair(pr, a, b, k_tiles, kpb); return; }
     // an MN-major tile is loaded in whole 128-byte atoms: a partial atom would never complete
     // the stage's transaction count
     if (b.mn && !tf32 && pr->BN % CH) { error(PPX_E_CONFIG, "MN-major B tile width must be a multiple of 64"); return; }
@@ -391,17 +480,28 @@ struct Builder {
 
   ppx_status launch() {
     if (!ok()) return status;
+    use_pair = want_pair && pair_shapes_ok();
+    BKf = use_pair ? ppx::PBK : BK;
+    if (use_pair) {
+      for (int i = 0; i < P.nprobs; ++i) {
+        Problem& pr = P.probs[i];
+        pr.m_tiles = (int)cdiv(pr.M, 2 * ppx::BM);
+        pr.BN = pick_bn(pr.nb_extent, prob_bmn[i] ? 128 : 32);
+        pr.npb = (int)cdiv(pr.nb_extent, pr.BN);
+      }
+    }
     auto count_tiles = [&]() {
       int t = 0;
       for (int i = 0; i < P.nprobs; ++i) t += P.probs[i].m_tiles * P.probs[i].nblk * P.probs[i].npb;
       return t;
     };
     // small launches: trade N-tile width for more CTAs (tcgen05 throughput per SM is N-invariant)
-    for (int guard = 0; guard < 4 && count_tiles() * 4 < ctx->num_sms * 3; ++guard) {
+    const int slots = use_pair ? ctx->num_sms / 2 : ctx->num_sms;
+    for (int guard = 0; guard < 4 && count_tiles() * 4 < slots * 3; ++guard) {
       bool changed = false;
       for (int i = 0; i < P.nprobs; ++i) {
         Problem& pr = P.probs[i];
-        const int gran = prob_bmn[i] ? CH : 32;
+        const int gran = use_pair ? (prob_bmn[i] ? 128 : 64) : (prob_bmn[i] ? CH : 32);
         if (pr.BN / 2 >= gran && (pr.BN / 2) % gran == 0 && (pr.BN / 2) % 16 == 0 && pr.nb_extent > pr.BN / 2) {
           pr.BN /= 2;
           pr.npb = (int)cdiv(pr.nb_extent, pr.BN);
@@ -419,9 +519,16 @@ struct Builder {
       tiles += P.probs[i].m_tiles * P.probs[i].nblk * P.probs[i].npb;
     }
     P.total_tiles = tiles;
+    P.dbg = (getenv("PPX_DEBUG_NOEPI") ? 1 : 0) | (getenv("PPX_DEBUG_NOWAIT") ? 2 : 0);
     if (tiles == 0) return PPX_OK;
-    int grid = tiles < ctx->num_sms ? tiles : ctx->num_sms;
-    cudaError_t e = tf32 ? ppx::launch_gemm<true>(P, grid, st) : ppx::launch_gemm<false>(P, grid, st);
+    cudaError_t e;
+    if (use_pair) {
+      const int clusters = tiles < ctx->num_sms / 2 ? tiles : ctx->num_sms / 2;
+      e = ppx::launch_gemm_pair(P, 2 * clusters, st);
+    } else {
+      int grid = tiles < ctx->num_sms ? tiles : ctx->num_sms;
+      e = tf32 ? ppx::launch_gemm<true>(P, grid, st) : ppx::launch_gemm<false>(P, grid, st);
+    }
     if (e != cudaSuccess) return fail(ctx, PPX_E_CUDA, "gemm launch: %s", cudaGetErrorString(e));
     return PPX_OK;
   }
@@ -449,6 +556,27 @@ cudaError_t launch_gemm(const GemmParams& P, int grid, cudaStream_t st) {
   }
   gemm_kernel<kTF32><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(P);
   return cudaGetLastError();
+}
+cudaError_t launch_gemm_pair(const GemmParams& P, int grid, cudaStream_t st) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PSMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = PSMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_pair_kernel, P);
 }
 template cudaError_t launch_gemm<true>(const GemmParams&, int, cudaStream_t);
 template cudaError_t launch_gemm<false>(const GemmParams&, int, cudaStream_t);
