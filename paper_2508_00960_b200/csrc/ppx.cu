@@ -26,6 +26,7 @@
 
 struct ppx_ctx {
   int world = 1, rank = 0, device = 0, num_sms = 148;
+  int reserved_sms = 0;   // SMs GEMM grids leave free for a concurrent collective
   ncclComm_t comm = nullptr;
   std::string err;
   // FP32-tier hi/lo split workspace: a pool of chunks, bump-allocated per call and reused by the
@@ -522,11 +523,12 @@ struct Builder {
     P.dbg = (getenv("PPX_DEBUG_NOEPI") ? 1 : 0) | (getenv("PPX_DEBUG_NOWAIT") ? 2 : 0);
     if (tiles == 0) return PPX_OK;
     cudaError_t e;
+    const int sms = ctx->num_sms - ctx->reserved_sms;
     if (use_pair) {
-      const int clusters = tiles < ctx->num_sms / 2 ? tiles : ctx->num_sms / 2;
+      const int clusters = tiles < sms / 2 ? tiles : sms / 2;
       e = ppx::launch_gemm_pair(P, 2 * clusters, st);
     } else {
-      int grid = tiles < ctx->num_sms ? tiles : ctx->num_sms;
+      int grid = tiles < sms ? tiles : sms;
       e = tf32 ? ppx::launch_gemm<true>(P, grid, st) : ppx::launch_gemm<false>(P, grid, st);
     }
     if (e != cudaSuccess) return fail(ctx, PPX_E_CUDA, "gemm launch: %s", cudaGetErrorString(e));
@@ -628,6 +630,12 @@ ppx_status ppx_destroy(ppx_ctx* ctx) {
 
 const char* ppx_last_error(const ppx_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 int32_t ppx_num_sms(const ppx_ctx* ctx) { return ctx ? ctx->num_sms : 0; }
+
+ppx_status ppx_set_reserved_sms(ppx_ctx* ctx, int32_t n) {
+  if (!ctx || n < 0 || n > ctx->num_sms - 2) return PPX_E_CONFIG;
+  ctx->reserved_sms = n;
+  return PPX_OK;
+}
 
 ppx_status ppx_reserve_workspace(ppx_ctx* ctx, int64_t bytes) {
   if (!ctx || bytes < 0) return PPX_E_CONFIG;

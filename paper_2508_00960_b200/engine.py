@@ -110,6 +110,10 @@ class PhantomEngine:
         if dtype == torch.float32:   # 3xTF32 hi/lo splits: reserve so graph capture never allocates
             per_call = 4 * B * s + 2 * p * B * ldk + 2 * T + 4 * s * ldk
             self.ctx.call("ppx_reserve_workspace", int(2 * 4 * per_call * 1.25) + (1 << 20))
+        self.comm_sms = int(os.environ.get("PPX_COMM_SMS", "0"))
+        # PPX_NOGROUP=1 launches every logical rank separately (emulates the R=1 launch shapes of an
+        # 8-GPU run on one GPU, for profiling)
+        self.group = 1 if os.environ.get("PPX_NOGROUP") else R
         self.graphs = [None, None]
         self.parity = 0
         self._keep = []   # ctypes structs of the launch being built
@@ -238,7 +242,9 @@ class PhantomEngine:
 
         def compress(l, h):
             ios = [self._io(jj, l, par, x=rows(self.Y[par][jj][l], h), ld_x=s) for jj in range(R)]
-            self._call("ppx_compress_n", pdt, R, self._ios(ios), Bh, self._gh(l, h), st)
+            for c in range(0, R, self.group):
+                self._call("ppx_compress_n", pdt, min(self.group, R - c), self._ios(ios[c:c + self.group]), Bh,
+                           self._gh(l, h), st)
             if self.world > 1:
                 self._join(S, self.comm_stream)
                 self._call("ppx_all_gather", pdt, self._gh(l, h), Bh * self.off["ldk"], R,
@@ -263,9 +269,10 @@ class PhantomEngine:
                         kw.update(aux=rows(self.D[jj][0], h), ld_aux=s, target=rows(self.Tgt[par][jj], h), ld_t=s,
                                   colsum=self.gbias[jj, l].data_ptr())
                     ios.append(self._io(jj, l, par, **kw))
-                self._call("ppx_forward_n", pdt, R, self._ios(ios), Bh, self.act.code, self._gh(l, h), int(last),
-                           1.0 / B if mean else 1.0, 0.5 / B if mean else 0.5,
-                           self.loss.data_ptr() if last else None, st)
+                for c in range(0, R, self.group):
+                    self._call("ppx_forward_n", pdt, min(self.group, R - c), self._ios(ios[c:c + self.group]), Bh,
+                               self.act.code, self._gh(l, h), int(last), 1.0 / B if mean else 1.0,
+                               0.5 / B if mean else 0.5, self.loss.data_ptr() if last else None, st)
                 if l + 1 < self.L:
                     compress(l + 1, h)
 
@@ -303,11 +310,16 @@ class PhantomEngine:
                                                 ctypes.pointer(self._update(jj, l + 1, par))))
                 per_rank.append(items)
             nprob = 2 + (1 if l < L - 1 else 0) if self.p > 1 else 1
-            per = max(1, 16 // nprob)
+            per = max(1, min(self.group, 16 // nprob))
             nl = -(-R // per)
             per = -(-R // nl)
+            # leave SMs to the reduce-scatter running on the comm stream under these GEMMs
+            if self.world > 1 and self.comm_sms:
+                self.ctx.call("ppx_set_reserved_sms", self.comm_sms)
             for c in range(0, R, per):
                 self._launch_wgrad([it for chunk in per_rank[c:c + per] for it in chunk], st)
+            if self.world > 1 and self.comm_sms:
+                self.ctx.call("ppx_set_reserved_sms", 0)
             if self.world > 1:
                 self._join(self.comm_stream, S)
             if l > 0:
@@ -319,7 +331,9 @@ class PhantomEngine:
                                         mask=self.Y[par][jj][l].data_ptr() if self.act is Activation.RELU else None,
                                         ld_m=s, received=self._received(l, j),
                                         colsum=self.gbias[jj, l - 1].data_ptr()))
-                self._call("ppx_backward_delta_n", pdt, R, self._ios(ios), B, self.act.code, st)
+                for c in range(0, R, self.group):
+                    self._call("ppx_backward_delta_n", pdt, min(self.group, R - c), self._ios(ios[c:c + self.group]),
+                               B, self.act.code, st)
                 cur = 1 - cur
         # d compressor of layer 0, all local ranks in one launch
         items = [_lib.WgradItem(ctypes.pointer(self._layer(jj, 0, par)), _lib.GRAD_COMP, B,
@@ -327,7 +341,8 @@ class PhantomEngine:
                                 self._received(0, self.local[jj]), None, ctypes.pointer(self._update(jj, 0, par)))
                  for jj in range(R)]
         if self.p > 1:
-            self._launch_wgrad(items, st)
+            for c in range(0, R, self.group):
+                self._launch_wgrad(items[c:c + self.group], st)
         # biases of all local ranks and layers in one elementwise launch
         kind = _lib.PPX_UPDATE_ADAM if self.optimizer == "adam" else _lib.PPX_UPDATE_SGD
         self._call("ppx_optimizer_step", kind, self.hyper.data_ptr(), self.bias.data_ptr(), self.gbias.data_ptr(),
