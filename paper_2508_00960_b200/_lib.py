@@ -14,7 +14,7 @@ import threading
 from .errors import (ConfigurationError, DeviceError, ProtocolError,
                      SequencingError, TrainingError)
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libppx.so")
+LIB_PATH = os.environ.get("PPX_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libppx.so")
 
 PPX_OK, PPX_E_CONFIG, PPX_E_PROTOCOL, PPX_E_SEQUENCING, PPX_E_NONFINITE, PPX_E_CUDA = range(6)
 PPX_BF16, PPX_FP32 = 0, 1

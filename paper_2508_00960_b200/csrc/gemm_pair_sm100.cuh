@@ -16,7 +16,7 @@ constexpr int PBK = 128;                         // K elements per stage (2 atom
 constexpr int PSTAGES = 3;
 constexpr int PA_STAGE = BM * 2 * ROW_BYTES;     // 32 KB: [2 K-atoms][128 rows][128 B]
 constexpr int PB_STAGE = 128 * 2 * ROW_BYTES;    // 32 KB: [2 K-atoms][<=128 rows][128 B]
-constexpr int PSMEM_BYTES = PSTAGES * (PA_STAGE + PB_STAGE) + 1024 + 256;
+constexpr int PSMEM_BYTES = PSTAGES * (PA_STAGE + PB_STAGE) + 1024 + 256 + COLSUM_BYTES;
 
 __device__ __forceinline__ void tma4_pair(const CUtensorMap* map, uint32_t bar, uint32_t dst, int c0, int c1, int c2,
                                           int c3) {
@@ -70,12 +70,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  float* cs_smem = reinterpret_cast<float*>(smem_gen + (sBar + 256 - base_u32));
+  for (int i = threadIdx.x; i < 2 * BN_MAX; i += NUM_THREADS) cs_smem[i] = 0.f;
   const uint32_t crank = cluster_ctarank();
   const bool leader = crank == 0;
   constexpr int CHA = 64;       // bf16 elements per 128-byte atom
   constexpr int KMMA = 16;      // K per tcgen05.mma (bf16)
 
-  if (warp == 0 && lane == 0) {
+  if (warp == W_TMA && lane == 0) {
     for (int i = 0; i < P.nmaps; ++i) prefetch_map(&P.maps[i]);
     for (int s = 0; s < PSTAGES; ++s) {
       mbar_init(full_bar(s), 1);
@@ -83,11 +85,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(tfull_bar(s), 1);
-      mbar_init(tempty_bar(s), 8);   // 4 epilogue warps in each CTA of the pair
+      mbar_init(tempty_bar(s), 2 * NUM_EPI_WARPS);   // the epilogue warps of both CTAs of the pair
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 2) {
+  if (warp == W_ALLOC) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
@@ -101,7 +103,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
   const int t0 = (int)(blockIdx.x >> 1);
   const int tstep = (int)(gridDim.x >> 1);
 
-  if (warp == 0) {
+  if (is_epi_warp(warp)) {
+    reg_alloc_epilogue();
+    epilogue_loop<2 * BM, true>(P, tmem_base, tfull_bar(0), tempty_bar(0), t0, tstep, crank, warp, lane, cs_smem);
+  } else {
+  reg_dealloc_mainloop();
+  if (warp == W_TMA) {
     // ===================== TMA producer (both CTAs) =====================
     if (lane == 0) {
       int stage = 0;
@@ -139,7 +146,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
+  } else if (warp == W_MMA) {
     // ===================== MMA issuer (leader CTA, one lane) =====================
     if (leader && lane == 0) {
       int stage = 0;
@@ -191,14 +198,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
       }
     }
     __syncwarp();
-  } else if (warp >= 4) {
-    epilogue_loop<2 * BM, true>(P, tmem_base, tfull_bar(0), tempty_bar(0), t0, tstep, crank, warp, lane);
+  }
   }
 
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
-  if (warp == 2) {
+  if (warp == W_ALLOC) {
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
   }
 }
