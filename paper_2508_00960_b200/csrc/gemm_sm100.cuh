@@ -117,6 +117,7 @@ struct Problem {
   int nblk;          // number of N blocks
   int BN;            // tile N (multiple of 16, <= 256)
   int m_tiles, npb;  // tiles along M, tiles per N block
+  int m_base;        // first row covered by this problem's tiles (a split-off tail of a problem)
   int tile_begin;    // prefix over problems
   int nsegs;
   Segment segs[MAX_SEGS];
@@ -130,6 +131,7 @@ struct alignas(64) GemmParams {
   int nprobs;
   int total_tiles;
   int dbg;             // debug: bit0 = skip the epilogue body (TMEM drain only by arrival)
+  unsigned long long* stats;   // debug (PPX_DEBUG_STATS): per-role wait / busy clock sums, else null
 };
 
 // ------------------------------------------------------------------------------------------
@@ -166,6 +168,14 @@ __device__ __forceinline__ uint64_t global_ns() {
   return t;
 }
 // Blocking wait with a watchdog: a pipeline bug traps after ~20 s instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity);
+// mbar_wait that adds the cycles spent to *acc when profiling statistics are on
+__device__ __forceinline__ void mbar_wait_t(uint32_t bar, uint32_t parity, bool on, unsigned long long& acc) {
+  if (!on) { mbar_wait(bar, parity); return; }
+  const unsigned long long c0 = clock64();
+  mbar_wait(bar, parity);
+  acc += clock64() - c0;
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const uint64_t t0 = global_ns();
@@ -227,6 +237,14 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// accumulator-drained signals: only the (already waited) TMEM loads must precede them, not the
+// epilogue's global stores, so the arrive is relaxed and never waits for stores to drain
+__device__ __forceinline__ void mbar_arrive_relaxed(uint32_t bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
 template <bool kTF32>
@@ -464,7 +482,7 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, int t) {
   int nt = local - mt * ntn;
   TileCoord c;
   c.prob = pi;
-  c.m0 = mt * MT;
+  c.m0 = pr.m_base + mt * MT;
   c.qn = nt / pr.npb;
   c.nin = (nt - c.qn * pr.npb) * pr.BN;
   return c;
@@ -487,6 +505,7 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
   auto tempty_bar = [&](int s) { return tempty0 + 8u * s; };
   const int wq = warp & 3;    // TMEM lane quadrant
   const int grp = warp >> 2;  // chunk parity drained by this warp
+  unsigned long long st_wait = 0, st_busy = 0, st_tmem = 0, st_body = 0;
   int iter = 0;
   for (int t = t0; t < total; t += tstep, ++iter) {
     TileCoord tc = tile_coord<MT>(P, t);
@@ -520,7 +539,8 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
         prefetch_row(E.adam_v, m_row + tc.nin, ncols);
       }
     }
-    mbar_wait(tfull_bar(as), aphase);
+    mbar_wait_t(tfull_bar(as), aphase, P.stats != nullptr, st_wait);
+    const unsigned long long c_busy = P.stats ? clock64() : 0ull;
     tc_fence_after();
     float loss_acc = 0.f;
     bool bad = false;
@@ -543,7 +563,9 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
         pre_issue(sa ? *sa : E.out, a_row + col0 + 64, nv1, sa && row_ok && c + 2 < nchunks && nv1 > 0, na);
       }
       float v[32];
+      const unsigned long long c_t0 = P.stats ? clock64() : 0ull;
       tmem_ld32(tmem_base + as * BN_MAX + c * 32 + ((uint32_t)(wq * 32) << 16), v);
+      if (P.stats) st_tmem += clock64() - c_t0;
       // full chunks (every row and column valid, the common case) compile without per-element masks
       auto body = [&](auto full_c) {
         constexpr bool F = decltype(full_c)::value;
@@ -624,8 +646,10 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
           }
         }
       };
+      const unsigned long long c_b0 = P.stats ? clock64() : 0ull;
       if (nvalid == 32 && rows_valid == 32) body(std::true_type{});
       else body(std::false_type{});
+      if (P.stats) st_body += clock64() - c_b0;
       pa = na;
     }
     if (flags & EP_LOSS) {
@@ -650,9 +674,16 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
     tc_fence_before();
     __syncwarp();
     if (lane == 0) {
-      if constexpr (kPair) mbar_arrive_cluster(mapa_shared(tempty_bar(as), 0));
-      else mbar_arrive(tempty_bar(as));
+      if constexpr (kPair) mbar_arrive_cluster_relaxed(mapa_shared(tempty_bar(as), 0));
+      else mbar_arrive_relaxed(tempty_bar(as));
     }
+    if (P.stats) st_busy += clock64() - c_busy;
+  }
+  if (P.stats && lane == 0) {
+    atomicAdd(P.stats + 0, st_wait);
+    atomicAdd(P.stats + 1, st_busy);
+    atomicAdd(P.stats + 7, st_tmem);
+    atomicAdd(P.stats + 8, st_body);
   }
 }
 

@@ -479,6 +479,36 @@ struct Builder {
     }
   }
 
+  // Wave-quantisation trim for the static tile schedule: when the last round of tiles would
+  // occupy at most half of the clusters, the trailing M-tile rows of the last problem move into
+  // a copy of that problem with half-width N tiles, so the last round runs twice as many
+  // half-length tiles (e.g. 256 tiles on 74 clusters: 3.5 tile-times instead of 4).
+  void split_tail(int clusters) {
+    if (clusters < 2 || P.nprobs < 1 || P.nprobs >= ppx::MAX_PROBS) return;
+    int T = 0;
+    for (int i = 0; i < P.nprobs; ++i) T += P.probs[i].m_tiles * P.probs[i].nblk * P.probs[i].npb;
+    const int rounds = T / clusters, rem = T % clusters;
+    if (rounds < 1 || rem == 0 || rem > clusters / 2) return;
+    const int li = P.nprobs - 1;
+    Problem& last = P.probs[li];
+    const int gran = prob_bmn[li] ? 128 : 64;
+    const int half = last.BN / 2;
+    if (half < gran || half % gran || half % 16 || last.nb_extent <= half) return;
+    const int ntn = last.nblk * last.npb;
+    const int rows = (int)cdiv(rem, ntn);
+    if (rows >= last.m_tiles) return;
+    const int ti = P.nprobs++;
+    Problem& tail = P.probs[ti];
+    tail = last;
+    last.m_tiles -= rows;
+    tail.m_base = last.m_base + last.m_tiles * 2 * ppx::BM;
+    tail.m_tiles = rows;
+    tail.BN = half;
+    tail.npb = (int)cdiv(tail.nb_extent, half);
+    pend[ti] = pend[li];
+    prob_bmn[ti] = prob_bmn[li];
+  }
+
   ppx_status launch() {
     if (!ok()) return status;
     use_pair = want_pair && pair_shapes_ok();
@@ -511,6 +541,7 @@ struct Builder {
       }
       if (!changed) break;
     }
+    if (use_pair && !getenv("PPX_NO_TAILSPLIT")) split_tail(ctx->num_sms / 2 - ctx->reserved_sms / 2);
     for (int i = 0; i < P.nprobs && ok(); ++i)
       for (const PendingSeg& ps : pend[i]) finalize(&P.probs[i], ps);
     if (!ok()) return status;
@@ -524,9 +555,24 @@ struct Builder {
     if (tiles == 0) return PPX_OK;
     cudaError_t e;
     const int sms = ctx->num_sms - ctx->reserved_sms;
+    static unsigned long long* dstats = nullptr;
+    const bool want_stats = getenv("PPX_DEBUG_STATS") != nullptr;
+    if (want_stats && !dstats) cudaMalloc(&dstats, 16 * sizeof(unsigned long long));
+    P.stats = want_stats ? dstats : nullptr;
+    if (want_stats) cudaMemsetAsync(dstats, 0, 16 * sizeof(unsigned long long), st);
     if (use_pair) {
       const int clusters = tiles < sms / 2 ? tiles : sms / 2;
       e = ppx::launch_gemm_pair(P, 2 * clusters, st);
+      if (want_stats) {
+        unsigned long long h[16];
+        cudaMemcpyAsync(h, dstats, sizeof(h), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        const double n = (double)(h[6] ? h[6] : 1), ne = 16.0 * n;   // MMA issuers; epilogue warps
+        fprintf(stderr, "[ppx stats] tiles=%d clusters=%d  per-MMA-warp kcyc: total %.1f tempty-wait %.1f full-wait %.1f | "
+                "producer empty-wait %.1f | per-epi-warp tfull-wait %.1f busy %.1f (tmem ld %.1f body %.1f)\n",
+                tiles, clusters, h[5] / n / 1e3, h[3] / n / 1e3, h[4] / n / 1e3, h[2] / (2 * n) / 1e3, h[0] / ne / 1e3,
+                h[1] / ne / 1e3, h[7] / ne / 1e3, h[8] / ne / 1e3);
+      }
     } else {
       int grid = tiles < sms ? tiles : sms;
       e = tf32 ? ppx::launch_gemm<true>(P, grid, st) : ppx::launch_gemm<false>(P, grid, st);
