@@ -120,7 +120,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
         const int bnc = pr.BN / 2;
         const uint32_t bytes = (uint32_t)(BM + bnc) * 2u * ROW_BYTES * 2u;   // both CTAs, 2 K-atoms each
         const int am0 = tc.m0 + (int)crank * BM;
-        const int bn0 = tc.nin + (int)crank * bnc;
+        // a spanning tile gives each CTA of the pair one whole N block; otherwise the two CTAs
+        // split one block's BN columns
+        const bool span = pr.nspan > 1;
+        const int bn0 = span ? tc.nin : tc.nin + (int)crank * bnc;
+        const int qb = span ? tc.qn + (int)crank : tc.qn;
         for (int sg = 0; sg < pr.nsegs; ++sg) {
           const Segment& seg = pr.segs[sg];
           const CUtensorMap* ma = &P.maps[seg.a.map];
@@ -134,7 +138,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
             const uint32_t da = sA + stage * PA_STAGE;
             const uint32_t db = sB + stage * PB_STAGE;
             const int slot_a = op_slot(seg.a, kblk, tc.qn);
-            const int slot_b = op_slot(seg.b, kblk, tc.qn);
+            const int slot_b = op_slot(seg.b, kblk, qb);
             if (!seg.a.mn) tma4_pair(ma, fb, da, 0, am0, kin / CHA, slot_a);
             else if (seg.a.atoms4d == 2) tma5_pair(ma, fb, da, am0 / CHA, kin / 8, slot_a);
             else tma4_pair(ma, fb, da, 0, kin, am0 / CHA, slot_a);

@@ -118,6 +118,7 @@ struct Problem {
   int BN;            // tile N (multiple of 16, <= 256)
   int m_tiles, npb;  // tiles along M, tiles per N block
   int m_base;        // first row covered by this problem's tiles (a split-off tail of a problem)
+  int nspan;         // 2-SM kernel: N blocks per tile (2 = each CTA of the pair owns one whole N block)
   int tile_begin;    // prefix over problems
   int nsegs;
   Segment segs[MAX_SEGS];
@@ -477,13 +478,14 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, int t) {
   while (pi + 1 < P.nprobs && t >= P.probs[pi + 1].tile_begin) ++pi;
   const Problem& pr = P.probs[pi];
   int local = t - pr.tile_begin;
-  int ntn = pr.nblk * pr.npb;
+  const int span = pr.nspan > 1 ? pr.nspan : 1;
+  int ntn = (pr.nblk + span - 1) / span * pr.npb;
   int mt = local / ntn;
   int nt = local - mt * ntn;
   TileCoord c;
   c.prob = pi;
   c.m0 = pr.m_base + mt * MT;
-  c.qn = nt / pr.npb;
+  c.qn = nt / pr.npb * span;
   c.nin = (nt - c.qn * pr.npb) * pr.BN;
   return c;
 }
@@ -518,7 +520,6 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
     rows_valid = rows_valid < 0 ? 0 : (rows_valid > 32 ? 32 : rows_valid);
     const int row = row0 + lane;
     const bool row_ok = lane < rows_valid;
-    const int oslot = tc.qn + (tc.qn >= E.out_skip ? 1 : 0);
     const uint32_t flags = E.flags;
     const bool upd = (flags & (EP_SGD | EP_ADAM)) != 0;
     // per-row input streamed one chunk ahead: target | fp32 master | ReLU mask | accumulated output
@@ -526,17 +527,33 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
                         : upd            ? &E.master
                         : (flags & EP_MASK) ? &E.mask
                         : (flags & EP_ACCUM) ? &E.out : nullptr;
-    const bool sa_slot = upd || sa == &E.out;
-    const long long a_row = sa ? (sa_slot ? (long long)oslot * sa->slot_stride : 0) + (long long)row * sa->ld : 0;
-    const long long o_row = (long long)oslot * E.out.slot_stride + (long long)row * E.out.ld;
-    const long long m_row = (long long)oslot * E.master.slot_stride + (long long)row * E.master.ld;
-    const int ncols = pr.nb_extent - tc.nin < pr.BN ? pr.nb_extent - tc.nin : pr.BN;
+    const long long a_ss = sa && (upd || sa == &E.out) ? sa->slot_stride : 0;
+    const long long a_rb = sa ? (long long)row * sa->ld : 0;
+    const long long o_rb = (long long)row * E.out.ld, m_rb = (long long)row * E.master.ld;
+    // chunk c -> (N block, column inside it): a spanning tile's two halves are consecutive N blocks
+    const int half = pr.nspan > 1 ? pr.BN / 2 : (1 << 30);
+    auto geom = [&](int c, int& col0, int& nvalid, int& oslot) {
+      const int h = (c * 32) / half;
+      const int q = tc.qn + h;
+      col0 = tc.nin + c * 32 - h * half;
+      nvalid = q < pr.nblk ? pr.nb_extent - col0 : 0;
+      nvalid = nvalid > 32 ? 32 : nvalid;
+      oslot = q + (q >= E.out_skip ? 1 : 0);
+    };
     const int nchunks = (P.dbg & 1) ? 0 : (pr.BN + 31) / 32;
-    if (row_ok && ncols > 0 && nchunks && grp == 0) {    // warm L2 with this row's inputs while the MMAs run
-      if (sa) prefetch_row(*sa, a_row + tc.nin, ncols);
-      if (flags & EP_ADAM) {
-        prefetch_row(E.adam_m, m_row + tc.nin, ncols);
-        prefetch_row(E.adam_v, m_row + tc.nin, ncols);
+    const int ncols = pr.nb_extent - tc.nin < pr.BN ? pr.nb_extent - tc.nin : pr.BN;   // non-spanning tiles
+    if (row_ok && nchunks && grp == 0) {    // warm L2 with this row's inputs while the MMAs run
+      for (int h = 0; h * half < pr.BN; ++h) {
+        int col0, nv, os;
+        geom(h * half / 32, col0, nv, os);
+        const int n = pr.nspan > 1 ? (nv > 0 ? pr.nb_extent - col0 : 0) : ncols;
+        if (n <= 0) continue;
+        if (sa) prefetch_row(*sa, os * a_ss + a_rb + col0, n);
+        if (flags & EP_ADAM) {
+          const long long mo = (long long)os * E.master.slot_stride + m_rb + col0;
+          prefetch_row(E.adam_m, mo, n);
+          prefetch_row(E.adam_v, mo, n);
+        }
       }
     }
     mbar_wait_t(tfull_bar(as), aphase, P.stats != nullptr, st_wait);
@@ -545,22 +562,26 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
     float loss_acc = 0.f;
     bool bad = false;
     Pre32 pa;
-    {
-      int nv0 = ncols - grp * 32;
-      nv0 = nv0 > 32 ? 32 : nv0;
-      pre_issue(sa ? *sa : E.out, a_row + tc.nin + grp * 32, nv0, sa && row_ok && nv0 > 0 && grp < nchunks, pa);
+    if (grp < nchunks) {
+      int col0, nv0, os;
+      geom(grp, col0, nv0, os);
+      pre_issue(sa ? *sa : E.out, os * a_ss + a_rb + col0, nv0, sa && row_ok && nv0 > 0, pa);
     }
     for (int c = grp; c < nchunks; c += 2) {
-      const int col0 = tc.nin + c * 32;
-      int nvalid = pr.nb_extent - col0;
-      nvalid = nvalid > 32 ? 32 : nvalid;
+      int col0, nvalid, oslot;
+      geom(c, col0, nvalid, oslot);
+      const long long a_row = (long long)oslot * a_ss + a_rb;
+      const long long o_row = (long long)oslot * E.out.slot_stride + o_rb;
+      const long long m_row = (long long)oslot * E.master.slot_stride + m_rb;
       const bool live = row_ok && nvalid > 0;
       const float bl = ((flags & EP_BIAS) && lane < nvalid) ? E.bias[col0 + lane] : 0.f;
       Pre32 na;
-      {
-        int nv1 = pr.nb_extent - col0 - 64;
-        nv1 = nv1 > 32 ? 32 : nv1;
-        pre_issue(sa ? *sa : E.out, a_row + col0 + 64, nv1, sa && row_ok && c + 2 < nchunks && nv1 > 0, na);
+      if (c + 2 < nchunks) {
+        int col1, nv1, os1;
+        geom(c + 2, col1, nv1, os1);
+        pre_issue(sa ? *sa : E.out, os1 * a_ss + a_rb + col1, nv1, sa && row_ok && nv1 > 0, na);
+      } else {
+        na.vec = false;
       }
       float v[32];
       const unsigned long long c_t0 = P.stats ? clock64() : 0ull;

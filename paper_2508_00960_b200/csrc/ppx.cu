@@ -479,6 +479,30 @@ struct Builder {
     }
   }
 
+  static int ptiles(const Problem& pr) {
+    const int span = pr.nspan > 1 ? pr.nspan : 1;
+    return pr.m_tiles * (int)cdiv(pr.nblk, span) * pr.npb;
+  }
+
+  // 2-SM kernel: a problem whose N blocks (slots) are each at most half a tile wide runs tiles
+  // that span two consecutive blocks, one per CTA (e.g. the 7 k-wide phantom slots of
+  // ppx_error_phantoms / the decompressor gradient: 256 x 256 tiles instead of 256 x 128)
+  void pick_span() {
+    for (int i = 0; i < P.nprobs; ++i) {
+      Problem& pr = P.probs[i];
+      pr.nspan = 1;
+      if (pr.nblk < 2 || pr.npb != 1 || (pr.epi.flags & (ppx::EP_COLSUM | ppx::EP_BIAS))) continue;
+      bool slots_n = !pend[i].empty();
+      for (const PendingSeg& ps : pend[i]) slots_n = slots_n && ps.b.slot_src == 2 && ps.a.slot_src != 2;
+      if (!slots_n) continue;
+      const int g = prob_bmn[i] ? 64 : 16;
+      const int half = (int)cdiv(pr.nb_extent, g) * g;
+      if (2 * half > ppx::BN_MAX) continue;
+      pr.nspan = 2;
+      pr.BN = 2 * half;
+    }
+  }
+
   // Wave-quantisation trim for the static tile schedule: when the last round of tiles would
   // occupy at most half of the clusters, the trailing M-tile rows of the last problem move into
   // a copy of that problem with half-width N tiles, so the last round runs twice as many
@@ -486,15 +510,15 @@ struct Builder {
   void split_tail(int clusters) {
     if (clusters < 2 || P.nprobs < 1 || P.nprobs >= ppx::MAX_PROBS) return;
     int T = 0;
-    for (int i = 0; i < P.nprobs; ++i) T += P.probs[i].m_tiles * P.probs[i].nblk * P.probs[i].npb;
+    for (int i = 0; i < P.nprobs; ++i) T += ptiles(P.probs[i]);
     const int rounds = T / clusters, rem = T % clusters;
     if (rounds < 1 || rem == 0 || rem > clusters / 2) return;
     const int li = P.nprobs - 1;
     Problem& last = P.probs[li];
     const int gran = prob_bmn[li] ? 128 : 64;
     const int half = last.BN / 2;
-    if (half < gran || half % gran || half % 16 || last.nb_extent <= half) return;
-    const int ntn = last.nblk * last.npb;
+    if (half < gran || half % gran || half % 16 || (last.nspan < 2 && last.nb_extent <= half)) return;
+    const int ntn = ptiles(last) / last.m_tiles;
     const int rows = (int)cdiv(rem, ntn);
     if (rows >= last.m_tiles) return;
     const int ti = P.nprobs++;
@@ -504,6 +528,7 @@ struct Builder {
     tail.m_base = last.m_base + last.m_tiles * 2 * ppx::BM;
     tail.m_tiles = rows;
     tail.BN = half;
+    tail.nspan = 1;   // a spanning tile's half is one whole N block
     tail.npb = (int)cdiv(tail.nb_extent, half);
     pend[ti] = pend[li];
     prob_bmn[ti] = prob_bmn[li];
@@ -520,10 +545,11 @@ struct Builder {
         pr.BN = pick_bn(pr.nb_extent, prob_bmn[i] ? 128 : 32);
         pr.npb = (int)cdiv(pr.nb_extent, pr.BN);
       }
+      if (!getenv("PPX_NO_SPAN")) pick_span();
     }
     auto count_tiles = [&]() {
       int t = 0;
-      for (int i = 0; i < P.nprobs; ++i) t += P.probs[i].m_tiles * P.probs[i].nblk * P.probs[i].npb;
+      for (int i = 0; i < P.nprobs; ++i) t += ptiles(P.probs[i]);
       return t;
     };
     // small launches: trade N-tile width for more CTAs (tcgen05 throughput per SM is N-invariant)
@@ -533,6 +559,12 @@ struct Builder {
       for (int i = 0; i < P.nprobs; ++i) {
         Problem& pr = P.probs[i];
         const int gran = use_pair ? (prob_bmn[i] ? 128 : 64) : (prob_bmn[i] ? CH : 32);
+        if (pr.nspan > 1) {
+          pr.nspan = 1;
+          pr.BN /= 2;
+          changed = true;
+          continue;
+        }
         if (pr.BN / 2 >= gran && (pr.BN / 2) % gran == 0 && (pr.BN / 2) % 16 == 0 && pr.nb_extent > pr.BN / 2) {
           pr.BN /= 2;
           pr.npb = (int)cdiv(pr.nb_extent, pr.BN);
@@ -548,7 +580,7 @@ struct Builder {
     int tiles = 0;
     for (int i = 0; i < P.nprobs; ++i) {
       P.probs[i].tile_begin = tiles;
-      tiles += P.probs[i].m_tiles * P.probs[i].nblk * P.probs[i].npb;
+      tiles += ptiles(P.probs[i]);
     }
     P.total_tiles = tiles;
     P.dbg = (getenv("PPX_DEBUG_NOEPI") ? 1 : 0) | (getenv("PPX_DEBUG_NOWAIT") ? 2 : 0);
