@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
           for (int kt = 0; kt < seg.k_tiles; ++kt) {
             const int kblk = kt / seg.kpb;
             const int kin = (kt - kblk * seg.kpb) * PBK;
-            mbar_wait_t(empty_bar(stage), phase ^ 1u, P.stats != nullptr, st_empty);
+            mbar_wait_t(empty_bar(stage), phase ^ 1u, kStats && P.stats != nullptr, st_empty);
             if (leader) mbar_expect_tx(full_bar(stage), bytes);
             const uint32_t fb = mapa_shared(full_bar(stage), 0);
             const uint32_t da = sA + stage * PA_STAGE;
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
           }
         }
       }
-      if (P.stats) atomicAdd(P.stats + 2, st_empty);
+      if (kStats && P.stats) atomicAdd(P.stats + 2, st_empty);
     }
     __syncwarp();
   } else if (warp == W_MMA) {
@@ -159,13 +159,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
       uint32_t phase = 0;
       int iter = 0;
       unsigned long long st_tempty = 0, st_full = 0;
-      const unsigned long long c_start = P.stats ? clock64() : 0ull;
+      const unsigned long long c_start = kStats && P.stats ? clock64() : 0ull;
       for (int t = t0; t < total; t += tstep, ++iter) {
         TileCoord tc = tile_coord<2 * BM>(P, t);
         const Problem& pr = P.probs[tc.prob];
         const int as = iter & 1;
         const uint32_t aphase = (iter >> 1) & 1;
-        mbar_wait_t(tempty_bar(as), aphase ^ 1u, P.stats != nullptr, st_tempty);
+        mbar_wait_t(tempty_bar(as), aphase ^ 1u, kStats && P.stats != nullptr, st_tempty);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + as * BN_MAX;
         const int bnc = pr.BN / 2;
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
             b_lbo = 1024; b_sbo = (bnc / CHA) * 1024; b_step = 2 * b_sbo; b_katom = 4 * b_step;
           } else { b_lbo = PBK * ROW_BYTES; b_sbo = 1024; b_step = KMMA * ROW_BYTES; b_katom = 4 * b_step; }
           for (int kt = 0; kt < seg.k_tiles; ++kt) {
-            mbar_wait_t(full_bar(stage), phase, P.stats != nullptr, st_full);
+            mbar_wait_t(full_bar(stage), phase, kStats && P.stats != nullptr, st_full);
             tc_fence_after();
             const uint32_t da = sA + stage * PA_STAGE;
             const uint32_t db = sB + stage * PB_STAGE;
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
         }
         commit_pair(tfull_bar(as));
       }
-      if (P.stats) {
+      if (kStats && P.stats) {
         atomicAdd(P.stats + 3, st_tempty);
         atomicAdd(P.stats + 4, st_full);
         atomicAdd(P.stats + 5, clock64() - c_start);

@@ -170,6 +170,12 @@ __device__ __forceinline__ uint64_t global_ns() {
 }
 // Blocking wait with a watchdog: a pipeline bug traps after ~20 s instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity);
+// per-role clock statistics (wait / busy cycles, PPX_DEBUG_STATS at run time) exist only in a
+// build with -DPPX_STATS=1: the counters cost registers the 40-register mainloop warps lack
+#ifndef PPX_STATS
+#define PPX_STATS 0
+#endif
+constexpr bool kStats = PPX_STATS != 0;
 // mbar_wait that adds the cycles spent to *acc when profiling statistics are on
 __device__ __forceinline__ void mbar_wait_t(uint32_t bar, uint32_t parity, bool on, unsigned long long& acc) {
   if (!on) { mbar_wait(bar, parity); return; }
@@ -556,8 +562,8 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
         }
       }
     }
-    mbar_wait_t(tfull_bar(as), aphase, P.stats != nullptr, st_wait);
-    const unsigned long long c_busy = P.stats ? clock64() : 0ull;
+    mbar_wait_t(tfull_bar(as), aphase, kStats && P.stats != nullptr, st_wait);
+    const unsigned long long c_busy = kStats && P.stats ? clock64() : 0ull;
     tc_fence_after();
     float loss_acc = 0.f;
     bool bad = false;
@@ -584,9 +590,9 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
         na.vec = false;
       }
       float v[32];
-      const unsigned long long c_t0 = P.stats ? clock64() : 0ull;
+      const unsigned long long c_t0 = kStats && P.stats ? clock64() : 0ull;
       tmem_ld32(tmem_base + as * BN_MAX + c * 32 + ((uint32_t)(wq * 32) << 16), v);
-      if (P.stats) st_tmem += clock64() - c_t0;
+      if (kStats && P.stats) st_tmem += clock64() - c_t0;
       // full chunks (every row and column valid, the common case) compile without per-element masks
       auto body = [&](auto full_c) {
         constexpr bool F = decltype(full_c)::value;
@@ -620,22 +626,22 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
             if (E.out.ptr) store32(E.out, ooff, nvalid, w);
           }
         } else if (flags & EP_LOSS) {
-          float tg[32], d[32];
+          float tg[32];   // target, then the output delta in place
           pre_finish(E.target, a_row + col0, nvalid, live, pa, tg);
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const float y = (flags & EP_RELU) ? fmaxf(v[i], 0.f) : v[i];
             const float diff = ok(i) ? (y - tg[i]) : 0.f;
             loss_acc += diff * diff;
-            d[i] = ((flags & EP_RELU) && !(v[i] > 0.f)) ? 0.f : diff * E.scale;
+            tg[i] = ((flags & EP_RELU) && !(v[i] > 0.f)) ? 0.f : diff * E.scale;
             v[i] = y;
           }
           if (live) {
             store32(E.out, ooff, nvalid, v);
-            store32(E.aux, (long long)row * E.aux.ld + col0, nvalid, d);
+            store32(E.aux, (long long)row * E.aux.ld + col0, nvalid, tg);
           }
           if (flags & EP_COLSUM) {
-            const float cs = warp_transpose_sum(d, lane);
+            const float cs = warp_transpose_sum(tg, lane);
             if (lane < nvalid) atomicAdd(cs_smem + as * BN_MAX + c * 32 + lane, cs);
           }
         } else {
@@ -667,10 +673,10 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
           }
         }
       };
-      const unsigned long long c_b0 = P.stats ? clock64() : 0ull;
+      const unsigned long long c_b0 = kStats && P.stats ? clock64() : 0ull;
       if (nvalid == 32 && rows_valid == 32) body(std::true_type{});
       else body(std::false_type{});
-      if (P.stats) st_body += clock64() - c_b0;
+      if (kStats && P.stats) st_body += clock64() - c_b0;
       pa = na;
     }
     if (flags & EP_LOSS) {
@@ -698,9 +704,9 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
       if constexpr (kPair) mbar_arrive_cluster_relaxed(mapa_shared(tempty_bar(as), 0));
       else mbar_arrive_relaxed(tempty_bar(as));
     }
-    if (P.stats) st_busy += clock64() - c_busy;
+    if (kStats && P.stats) st_busy += clock64() - c_busy;
   }
-  if (P.stats && lane == 0) {
+  if (kStats && P.stats && lane == 0) {
     atomicAdd(P.stats + 0, st_wait);
     atomicAdd(P.stats + 1, st_busy);
     atomicAdd(P.stats + 7, st_tmem);
