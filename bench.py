@@ -422,15 +422,20 @@ def main():
         q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         q0.record(S)
         ready = eng.load_batch_async(xh, th, eng.parity)
+        prev_done = None
         for i in range(args.steps):
             S.wait_event(ready)
             par = eng.parity
             eng.step(graph=use_graph)
             done = torch.cuda.Event()
             done.record(S)
-            eng.copy_stream.wait_event(done)            # next parity's buffers are free again
             if i + 1 < args.steps:
+                # the next batch goes into the other parity's buffers, last read by step i-1:
+                # its H2D overlaps step i
+                if prev_done is not None:
+                    eng.copy_stream.wait_event(prev_done)
                 ready = eng.load_batch_async(xh, th, 1 - par)
+            prev_done = done
             eng.read_loss()                              # D2H of the step's loss (+ non-finite flag)
         q1.record(S)
         barrier()

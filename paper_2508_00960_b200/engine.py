@@ -43,6 +43,12 @@ def pp_forward_flops(n: int, p: int, k: int, layers: int, batch: int) -> int:
     return 2 * layers * batch * s * (s + p * k)
 
 
+def _dist_barrier():
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+
+
 class PhantomEngine:
     def __init__(self, n: int, p: int, k: int, layers: int, batch: int, *, world: int = 1, rank: int = 0,
                  device: int = 0, uid: bytes | None = None, activation=Activation.RELU, reduction: str = "mean",
@@ -165,11 +171,12 @@ class PhantomEngine:
                 self.bias[jj, l].copy_(torch.as_tensor(get("bias"), dtype=torch.float64))
         self.refresh_compute_copy()
 
-    def layer_views(self, jj, l):
-        """Reference-shaped views (local, compressor, {src: decompressor}, bias) of one shard."""
+    def layer_views(self, jj, l, master=None, bias=None):
+        """Reference-shaped views (local, compressor, {src: decompressor}, bias) of one shard
+        (of the fp32 master, or of another flat tensor in the same layout, e.g. Adam moments)."""
         s, k, p, off = self.s, self.k, self.p, self.off
         lds, ldk = off["lds"], off["ldk"]
-        m = self.master[jj, l]
+        m = self.master[jj, l] if master is None else master
         j = self.local[jj]
         decs = {}
         for q in range(p - 1):
@@ -177,7 +184,21 @@ class PhantomEngine:
             base = off["dec"] + q * s * ldk
             decs[i] = m[base:base + s * ldk].view(s, ldk)[:, :k]
         return {"local": m[0:s * lds].view(s, lds)[:, :s], "compressor": m[off["comp"]:off["comp"] + k * lds]
-                .view(k, lds)[:, :s], "decompressors": decs, "bias": self.bias[jj, l]}
+                .view(k, lds)[:, :s], "decompressors": decs, "bias": self.bias[jj, l] if bias is None else bias}
+
+    def save_checkpoint(self, path, seed: int = 0, *, optimizer_state: bool = False):
+        """PSHARD01 checkpoint of the weights (+ optimizer sidecar): every process writes its own
+        logical ranks in place (checkpoint.py)."""
+        from . import checkpoint
+        bar = _dist_barrier if self.world > 1 else None
+        fn = checkpoint.save_state if optimizer_state else checkpoint.save_engine
+        fn(path, self, seed, create=self.rank == 0, barrier=bar)
+
+    def load_checkpoint(self, path, *, optimizer_state: bool = False) -> int:
+        from . import checkpoint
+        seed = (checkpoint.load_state if optimizer_state else checkpoint.load_engine)(path, self)
+        torch.cuda.synchronize()
+        return seed
 
     # ------------------------------------------------------------------------------------------
     def _layer(self, jj, l, par):
