@@ -333,3 +333,141 @@ def train(config: TrainConfig, data: Dataset, comm_model=None, rates=None) -> Tr
     return TrainResult(epochs_run=epochs_run, iterations_run=epochs_run * iters_per_epoch, converged=converged,
                        final_loss=history[-1] if history else float("inf"), loss_history=history,
                        cost={"seconds": elapsed, "records": len(comm.records)})
+
+
+# ----------------------------------------------------------------------------------------------
+# on-device training loops: the fused engine runs the reference's TrainConfig
+# semantics — contiguous mini-batches in order, pre-update iteration losses, epoch loss = mean
+# of iteration losses, stop at target (training.py:276-309) — with measured time and NVML energy
+# ----------------------------------------------------------------------------------------------
+def _shard_batches(data: Dataset, s: int, ranks, dtype):
+    """Per logical rank, the (samples, s) row-major view of its feature rows."""
+    x = data.inputs.to(dtype)
+    y = data.targets.to(dtype)
+    return ([x[j * s:(j + 1) * s].t() for j in ranks], [y[j * s:(j + 1) * s].t() for j in ranks])
+
+
+def _reference_rows(config: TrainConfig, ranks):
+    from .phantom import _reference_init_arrays
+    s = config.n // config.p
+    rows = {}
+    for j in ranks:
+        row = []
+        for l in range(config.layers):
+            local, comp, decs = _reference_init_arrays(config.n, config.p, config.k, config.layers, config.seed, j, l)
+            row.append({"local": local, "compressor": comp, "decompressors": decs, "bias": np.zeros(s)})
+        rows[j] = row
+    return rows
+
+
+def train_engine(config: TrainConfig, data: Dataset, *, world: int = 1, rank: int = 0, device: int = 0,
+                 uid: bytes | None = None, init: str = "reference", graphs: bool = True) -> TrainResult:
+    """training.py:312-378 (PP mode) on the fused engine: this process owns p/world logical ranks.
+    cost = {seconds, joules (this GPU), samples_per_s, iterations}."""
+    from .energy import EnergyMeter
+    from .engine import PhantomEngine
+    config.validate()
+    if config.mode != "pp":
+        return train_tp_engine(config, data, world=world, rank=rank, device=device, uid=uid, graphs=graphs)
+    if data.inputs.shape[0] != config.n:
+        raise ConfigurationError(f"dataset width {data.inputs.shape[0]} does not match n={config.n}")
+    samples = data.sample_count
+    batch = config.batch or samples
+    if batch > samples or samples % batch != 0:
+        raise ConfigurationError(f"batch={batch} must divide the sample count {samples}")
+    iters = samples // batch
+    eng = PhantomEngine(config.n, config.p, config.k, config.layers, batch, world=world, rank=rank, device=device,
+                        uid=uid, activation=config.activation, reduction=config.loss_reduction,
+                        optimizer=config.optimizer, lr=config.lr, dtype=config.dtype, seed=config.seed)
+    try:
+        if init == "reference":
+            eng.load_params(_reference_rows(config, eng.local))
+        xs, ys = _shard_batches(data, config.n // config.p, eng.local, config.dtype)
+        history, converged, it_done, it_losses = [], False, 0, []
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with EnergyMeter(device) as meter:
+            for epoch in range(config.max_epochs):
+                losses = []
+                for it in range(iters):
+                    sl = slice(it * batch, (it + 1) * batch)
+                    eng.set_batch([x[sl] for x in xs], [y[sl] for y in ys])
+                    use_graph = graphs and it_done > 0
+                    if use_graph and eng.graphs[0] is None:
+                        eng.capture()
+                    eng.step(graph=use_graph)
+                    loss = eng.read_loss()
+                    if not math.isfinite(loss):
+                        raise TrainingError(f"loss diverged to {loss} at epoch {epoch}")
+                    losses.append(loss)
+                    it_losses.append(loss)
+                    it_done += 1
+                epoch_loss = float(np.mean(losses))
+                history.append(epoch_loss)
+                if config.target_loss is not None and epoch_loss <= config.target_loss:
+                    converged = True
+                    break
+            torch.cuda.synchronize()
+        elapsed = time.perf_counter() - t0
+    finally:
+        eng.close()
+    return TrainResult(epochs_run=len(history), iterations_run=it_done, converged=converged,
+                       final_loss=history[-1] if history else float("inf"), loss_history=history,
+                       cost={"seconds": elapsed, "joules": meter.joules, "iterations": it_done,
+                             "samples_per_s": it_done * batch / elapsed if elapsed > 0 else None,
+                             "iteration_losses": it_losses})
+
+
+def train_tp_engine(config: TrainConfig, data: Dataset, *, world: int = 1, rank: int = 0, device: int = 0,
+                    uid: bytes | None = None, graphs: bool = True) -> TrainResult:
+    """The Megatron comparison pipeline under the same loop (SGD, mean or sum reduction): the
+    dense model of tensor_parallel.full_layer_weight (the reference's TP init), p = world GPUs."""
+    from .energy import EnergyMeter
+    from .tensor_parallel import TPEngine, full_layer_weight
+    config.validate()
+    if config.optimizer != "sgd":
+        raise ConfigurationError("the TP engine trains with SGD")
+    samples = data.sample_count
+    batch = config.batch or samples
+    if batch > samples or samples % batch != 0:
+        raise ConfigurationError(f"batch={batch} must divide the sample count {samples}")
+    iters = samples // batch
+    eng = TPEngine(config.n, config.layers, batch, world=world, rank=rank, device=device, uid=uid, lr=config.lr,
+                   dtype=config.dtype, seed=config.seed, reduction=config.loss_reduction)
+    try:
+        eng.load_full_weights([full_layer_weight(config.n, l, config.seed) for l in range(config.layers)])
+        x = data.inputs.to(config.dtype).t()
+        y = data.targets.to(config.dtype).t()
+        history, converged, it_done, it_losses = [], False, 0, []
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with EnergyMeter(device) as meter:
+            for epoch in range(config.max_epochs):
+                losses = []
+                for it in range(iters):
+                    sl = slice(it * batch, (it + 1) * batch)
+                    eng.set_batch(x[sl], y[sl])
+                    use_graph = graphs and it_done > 0
+                    if use_graph and eng.graphs[0] is None:
+                        eng.capture()
+                    eng.step(graph=use_graph)
+                    loss = eng.read_loss()
+                    if not math.isfinite(loss):
+                        raise TrainingError(f"loss diverged to {loss} at epoch {epoch}")
+                    losses.append(loss)
+                    it_losses.append(loss)
+                    it_done += 1
+                epoch_loss = float(np.mean(losses))
+                history.append(epoch_loss)
+                if config.target_loss is not None and epoch_loss <= config.target_loss:
+                    converged = True
+                    break
+            torch.cuda.synchronize()
+        elapsed = time.perf_counter() - t0
+    finally:
+        eng.close()
+    return TrainResult(epochs_run=len(history), iterations_run=it_done, converged=converged,
+                       final_loss=history[-1] if history else float("inf"), loss_history=history,
+                       cost={"seconds": elapsed, "joules": meter.joules, "iterations": it_done,
+                             "samples_per_s": it_done * batch / elapsed if elapsed > 0 else None,
+                             "iteration_losses": it_losses})
