@@ -471,3 +471,23 @@ def train_tp_engine(config: TrainConfig, data: Dataset, *, world: int = 1, rank:
                        cost={"seconds": elapsed, "joules": meter.joules, "iterations": it_done,
                              "samples_per_s": it_done * batch / elapsed if elapsed > 0 else None,
                              "iteration_losses": it_losses})
+
+
+def gen_dataset_device(n: int, samples: int, seed: int, device=None, dtype=torch.bfloat16) -> Dataset:
+    """gen_dataset's teacher task drawn with the device generator (N(0,1) teacher and inputs,
+    targets relu(teacher . relu(x)) on the tensor cores) for widths where the reference's host
+    Philox draws are too slow; same distribution, not the same bits."""
+    if n < 1 or samples < 1:
+        raise ConfigurationError("n and samples must be >= 1")
+    dev = torch.device(device or "cuda")
+    g = torch.Generator(device=dev)
+    g.manual_seed(int(seed) & 0x7FFFFFFF)
+    teacher = torch.randn((n, n), generator=g, device=dev).to(dtype)
+    x = torch.randn((n, samples), generator=g, device=dev).to(dtype)
+    hidden = torch.clamp_min(x, 0)
+    t = torch.empty((samples, n), dtype=dtype, device=dev)
+    for c in range(0, samples, 8192):
+        e = min(samples, c + 8192)
+        t[c:e] = kernels.gemm(hidden[:, c:e], teacher, transpose_a=True, transpose_b=True, out_dtype=dtype,
+                              relu=True)
+    return Dataset(x, t.t(), teacher, seed)
