@@ -176,6 +176,12 @@ ppx_status ppx_output_delta(ppx_ctx* ctx, ppx_dtype dt, int32_t B, int32_t s, pp
 ppx_status ppx_error_phantoms(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B,
                               const void* delta, int64_t ld_d, void* contrib, int32_t accumulate,
                               void* stream);
+/* phantom.py:199-205 for the n logical ranks one GPU owns (io[j].layer ascending, io[j].x =
+   delta_j): slot i of contrib = sum_{j != i} delta_j . D_{i->j}, summed in the fp32 accumulator
+   in ascending rank order, every slot with at least one contributor OVERWRITTEN (no zeroing
+   pass, no accumulate launches); slots without a contributor are left untouched. */
+ppx_status ppx_error_phantoms_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B,
+                                void* contrib, void* stream);
 
 /* collectives.py:122-127 / 345-357 — in-place reduce-scatter of the contribution slots: after
    it, slot j of `contrib` (for this GPU's local ranks) is the sum over all GPUs. */

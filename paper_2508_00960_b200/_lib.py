@@ -85,6 +85,7 @@ _SIGS = {
     "ppx_output_delta": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _i64, _vp, _i64, _vp, _i64,
                                 _vp, _i64, _f32, _f32, _fp, _vp]),
     "ppx_error_phantoms": (_i32, [_vp, _i32, ctypes.POINTER(Layer), _i32, _vp, _i64, _vp, _i32, _vp]),
+    "ppx_error_phantoms_n": (_i32, [_vp, _i32, _i32, ctypes.POINTER(RankIO), _i32, _vp, _vp]),
     "ppx_reduce_scatter": (_i32, [_vp, _i32, _vp, _i64, _i32, _vp]),
     "ppx_all_reduce_f32": (_i32, [_vp, _fp, _i64, _vp]),
     "ppx_all_reduce": (_i32, [_vp, _i32, _vp, _i64, _vp]),

@@ -54,7 +54,7 @@ __device__ __forceinline__ void reg_dealloc_mainloop() { asm volatile("setmaxnre
 constexpr int TMEM_COLS = 512;    // 2 accumulator stages x 256 fp32 columns
 constexpr int MAX_MAPS = 40;
 constexpr int MAX_PROBS = 16;
-constexpr int MAX_SEGS = 6;
+constexpr int MAX_SEGS = 8;
 constexpr int COLSUM_BYTES = 2 * BN_MAX * 4;     // per-CTA column-sum staging, double-buffered by tile parity
 constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 /*align*/ + 256 /*barriers*/ + COLSUM_BYTES;
 
@@ -134,6 +134,7 @@ struct alignas(64) GemmParams {
   int dbg;             // debug: bit0 = skip the epilogue body (TMEM drain only by arrival)
   unsigned long long* stats;   // debug (PPX_DEBUG_STATS): per-role wait / busy clock sums, else null
 };
+static_assert(sizeof(GemmParams) <= 32764, "kernel parameter space");
 
 // ------------------------------------------------------------------------------------------
 // PTX helpers

@@ -883,6 +883,63 @@ ppx_status ppx_error_phantoms(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, in
   return b.launch();
 }
 
+// Grouped error compression for the n logical ranks one GPU owns (phantom.py:199-205): output
+// slot i = sum over contributing ranks j != i (ascending) of delta_j . D_{i->j}, as ONE
+// K-concatenated problem per slot (segment j reads D_{i->j} = slot i - (i > j) of rank j's
+// decompressor stack), so the ranks' contributions are summed in the fp32 accumulator instead
+// of n accumulate launches.  Slots without a contributor are not written.  Falls back to the
+// per-rank accumulate launches when a slot would need more than MAX_SEGS segments (or 3xTF32).
+ppx_status ppx_error_phantoms_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B,
+                                void* contrib, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (n < 1 || !io || B < 1 || !contrib) return fail(ctx, PPX_E_CONFIG, "ppx_error_phantoms_n: bad arguments");
+  for (int j = 0; j < n; ++j) {
+    const ppx_layer* L = io[j].layer;
+    if (bad_layer(L) || !io[j].x || L->s != io[0].layer->s || L->k != io[0].layer->k || L->p != io[0].layer->p ||
+        (j && L->rank <= io[j - 1].layer->rank))
+      return fail(ctx, PPX_E_CONFIG, "ppx_error_phantoms_n: ranks must share (s, k, p) and ascend");
+  }
+  const int p = io[0].layer->p, s = io[0].layer->s, k = io[0].layer->k;
+  if (p < 2) return PPX_OK;
+  Flat f(s, k, p);
+  const int es = dt == PPX_FP32 ? 4 : 2;
+  if (n == 1 || dt == PPX_FP32 || n > ppx::MAX_SEGS) {
+    if (n > 1) {
+      cudaError_t e = cudaMemsetAsync(contrib, 0, (size_t)p * B * f.ldk * es, (cudaStream_t)stream);
+      if (e != cudaSuccess) return fail(ctx, PPX_E_CUDA, "error_phantoms_n: %s", cudaGetErrorString(e));
+    }
+    for (int j = 0; j < n; ++j) {
+      ppx_status st = ppx_error_phantoms(ctx, dt, io[j].layer, B, io[j].x, io[j].ld_x, contrib, n > 1, stream);
+      if (st != PPX_OK) return st;
+    }
+    return PPX_OK;
+  }
+  int i = 0;
+  while (i < p) {
+    Builder b(ctx, dt, stream);
+    const int kt = (int)cdiv(s, b.BK);
+    for (; i < p && b.P.nprobs < ppx::MAX_PROBS - 1; ++i) {
+      int nseg = 0;
+      for (int j = 0; j < n; ++j) nseg += io[j].layer->rank != i;
+      if (!nseg) continue;
+      Problem* pr = b.new_problem(B, k, 1, true);
+      for (int j = 0; j < n; ++j) {
+        const ppx_layer* L = io[j].layer;
+        if (L->rank == i) continue;
+        Opnd a{view2(io[j].x, B, s, io[j].ld_x)};
+        Opnd d{view3(elem(dt, L->w, f.dec), p - 1, s, k, f.ldk, (int64_t)s * f.ldk)};
+        d.mn = 1;
+        d.slot_base = i - (i > L->rank ? 1 : 0);
+        b.add_segment(pr, a, d, kt, kt);
+      }
+      if (pr) pr->epi.out = t2((char*)contrib + (int64_t)i * B * f.ldk * es, f.ldk, 0);
+    }
+    ppx_status st = b.launch();
+    if (st != PPX_OK) return st;
+  }
+  return PPX_OK;
+}
+
 static ncclDataType_t nccl_type(ppx_dtype dt) { return dt == PPX_FP32 ? ncclFloat32 : ncclBfloat16; }
 
 ppx_status ppx_all_gather(ppx_ctx* ctx, ppx_dtype dt, void* phantoms, int64_t slot_elems, int32_t local_ranks,

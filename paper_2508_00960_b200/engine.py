@@ -221,7 +221,7 @@ class PhantomEngine:
         return self.H[l].data_ptr() + j * self.B * self.off["ldk"] * self.H[l].element_size()
 
     _KERNEL_CALLS = {"ppx_compress", "ppx_forward_update", "ppx_forward_output", "ppx_error_phantoms", "ppx_wgrad",
-                     "ppx_backward_delta", "ppx_optimizer_step", "ppx_compress_n", "ppx_forward_n",
+                     "ppx_backward_delta", "ppx_optimizer_step", "ppx_compress_n", "ppx_forward_n", "ppx_error_phantoms_n",
                      "ppx_backward_delta_n"}
 
     def _call(self, name, *args):
@@ -308,11 +308,19 @@ class PhantomEngine:
         esz = self.H[0].element_size()
         cur = 0
         for l in range(L - 1, -1, -1):
-            if R > 1:  # several local ranks accumulate into the same contribution slots
+            if self.group >= R and not os.environ.get("PPX_K3_PERRANK"):
+                # one launch: slot i = sum_{local j != i} delta_j . D_{i->j}, every slot with a
+                # contributor overwritten; with R = 1 the own slot has none and still holds the
+                # previous step's in-place reduce-scatter result, so it is zeroed first
+                if R == 1 and self.world > 1:
+                    self._call("ppx_zero", self._received(l, self.local[0]), slot * esz, st)
+                ios = [self._io(jj, l, par, x=self.D[jj][cur].data_ptr(), ld_x=s) for jj in range(R)]
+                self._call("ppx_error_phantoms_n", pdt, R, self._ios(ios), B, self.H[l].data_ptr(), st)
+            else:   # PPX_NOGROUP profiling: per-rank launches accumulating into zeroed slots
                 self._call("ppx_zero", self.H[l].data_ptr(), self.H[l].numel() * esz, st)
-            for jj in range(R):
-                self._call("ppx_error_phantoms", pdt, ctypes.byref(self._layer(jj, l, par)), B,
-                           self.D[jj][cur].data_ptr(), s, self.H[l].data_ptr(), int(R > 1), st)
+                for jj in range(R):
+                    self._call("ppx_error_phantoms", pdt, ctypes.byref(self._layer(jj, l, par)), B,
+                               self.D[jj][cur].data_ptr(), s, self.H[l].data_ptr(), 1, st)
             if self.world > 1:
                 self._join(S, self.comm_stream)
                 self._call("ppx_reduce_scatter", pdt, self.H[l].data_ptr(), slot, R, self.comm_stream.cuda_stream)

@@ -37,3 +37,54 @@ def test_gemm_layouts(dtype, ta, tb, shape):
     err = (out - ref).norm() / ref.norm().clamp_min(1e-30)
     tol = 1e-5 if dtype == torch.float32 else 1e-5  # inputs are exactly representable; fp32 accumulate
     assert err.item() < tol, f"normwise error {err.item():.3e}"
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("s,k,p,R,B", [(256, 128, 8, 8, 512), (256, 128, 8, 3, 256), (128, 32, 4, 4, 64),
+                                       (256, 64, 4, 2, 200), (192, 128, 8, 1, 256)])
+def test_error_phantoms_grouped(dtype, s, k, p, R, B):
+    """ppx_error_phantoms_n (phantom.py:199-205 for R local ranks in one launch): slot i =
+    sum_{j local, j != i} delta_j . D_{i->j}, vs a torch fp32 reference; slots without a
+    contributor keep their previous contents."""
+    import ctypes
+    from paper_2508_00960_b200 import _lib, kernels
+    from paper_2508_00960_b200.core import flat_offsets
+    off = flat_offsets(s, k, p)
+    g = torch.Generator(device="cuda").manual_seed(s + 7 * k + 13 * p + R)
+    ranks = list(range(p - R, p)) if R < p else list(range(p))
+    w = [torch.randn(off["total"], device="cuda", generator=g).to(dtype) for _ in ranks]
+    master = [torch.zeros(off["total"], device="cuda") for _ in ranks]
+    bias = [torch.zeros(s, device="cuda") for _ in ranks]
+    delta = [torch.randn(B, s, device="cuda", generator=g).to(dtype) for _ in ranks]
+    ldk = off["ldk"]
+    contrib = torch.full((p, B, ldk), 7.0, device="cuda", dtype=dtype)
+    keep = []
+    ios = []
+    for jj, j in enumerate(ranks):
+        L = _lib.Layer(s, k, p, j, w[jj].data_ptr(), master[jj].data_ptr(), bias[jj].data_ptr())
+        keep.append(L)
+        io = _lib.RankIO()
+        io.layer = ctypes.pointer(L)
+        io.x = delta[jj].data_ptr()
+        io.ld_x = s
+        ios.append(io)
+    arr = (_lib.RankIO * len(ios))(*ios)
+    ctx = kernels.ctx_for(contrib)
+    ctx.call("ppx_error_phantoms_n", kernels.ppx_dtype(dtype), len(ranks), arr, B, contrib.data_ptr(),
+             torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for i in range(p):
+        contributors = [jj for jj, j in enumerate(ranks) if j != i]
+        if not contributors:
+            assert torch.all(contrib[i] == 7.0)
+            continue
+        ref = torch.zeros(B, k, device="cuda")
+        for jj in contributors:
+            j = ranks[jj]
+            slot = i - (1 if i > j else 0)
+            D = w[jj][off["dec"]:off["bias"]].view(p - 1, s, ldk)[slot, :, :k].float()
+            ref += delta[jj].float() @ D
+        got = contrib[i, :, :k].float()
+        err = ((got - ref).norm() / ref.norm()).item()
+        tol = 1e-5 if dtype == torch.float32 else 1e-2   # bf16 output rounding
+        assert err < tol, (i, err)

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--dtype", default="fp32")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--graph", type=int, default=1)
+    ap.add_argument("--p", type=int, default=4)
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -26,7 +27,7 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     uid = [_lib.Context.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
-    n, p, k, L, B, lr = 512, 4, 32, 3, 64, 3e-3
+    n, p, k, L, B, lr = 512, args.p, 32, 3, 64, 3e-3
     dtype = torch.float32 if args.dtype == "fp32" else torch.bfloat16
     tol = 1e-4 if args.dtype == "fp32" else 2e-2
     model = po.init_phantom_model(n, p, k, L, 3)
