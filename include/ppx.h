@@ -163,6 +163,26 @@ ppx_status ppx_forward_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_i
 ppx_status ppx_backward_delta_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B,
                                 ppx_act act_prev, void* stream);
 
+/* ---- NVLink peer memory: the phantom all-gather (collectives.py:115-120, 337-339) as direct
+   stores from the compression GEMM's epilogue into every peer's phantom buffer, with per-layer
+   flags instead of an NCCL kernel.  Regions come from ppx_peer_alloc (cudaMalloc + IPC handle,
+   zero-filled, freed by ppx_destroy); the 64-byte handles are exchanged by the caller (any
+   channel) and mapped with ppx_peer_open (closed by ppx_destroy). ----------------------------- */
+ppx_status ppx_peer_alloc(ppx_ctx* ctx, int64_t bytes, void** ptr, uint8_t handle[64]);
+ppx_status ppx_peer_open(ppx_ctx* ctx, const uint8_t handle[64], void** peer_ptr);
+/* ppx_compress_n whose epilogue also writes each phantom tile at the same offset of the n_peers
+   buffers peer_phantoms[r] (peer mappings of the other GPUs' phantom buffers). */
+ppx_status ppx_compress_push(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B,
+                             void* phantoms, int32_t n_peers, void* const* peer_phantoms, void* stream);
+/* *counter += 1, then every flags[i] (an int32 in a peer's region) = *counter (release, system
+   scope).  Stream-ordered after the pushes it publishes. */
+ppx_status ppx_peer_signal(ppx_ctx* ctx, int32_t n, int32_t* const* flags, int32_t* counter, void* stream);
+/* *counter += 1, then wait until every flags[i] (local int32s written by the peers) >= *counter
+   (acquire, system scope).  After PPX_PEER_TIMEOUT_S seconds (default 30) it sets bit 1 of *bad
+   and returns instead of hanging. */
+ppx_status ppx_peer_wait(ppx_ctx* ctx, int32_t n, int32_t* const* flags, int32_t* counter, int32_t* bad,
+                         void* stream);
+
 /* phantom.py:169-182 (+ training.py:66-69 scaling) — standalone output delta and loss partial.
    `pre` is the pre-activation (or the layer output: ReLU'(pre) == (y > 0)). */
 ppx_status ppx_output_delta(ppx_ctx* ctx, ppx_dtype dt, int32_t B, int32_t s, ppx_act act,

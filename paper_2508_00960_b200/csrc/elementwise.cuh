@@ -204,4 +204,60 @@ inline cudaError_t launch_relu_mask(bool f32, int rows, int cols, void* x, int64
   return cudaGetLastError();
 }
 
+
+// ---- NVLink peer signalling (phantom exchange without NCCL) ------------------------------------
+// Each GPU keeps per-(layer, source) int32 flags in IPC-shared memory and two local counters per
+// layer that advance once per use in lockstep on every GPU: the sender stores its new counter
+// value into every peer's flag after its phantom stores; the receiver waits until every source's
+// flag reached its own new counter value.  Graph-replay safe (no resets); a receiver that waits
+// longer than `timeout_ns` sets bit 1 of *bad and stops waiting (never hangs the GPU).
+constexpr int MAX_PEERS = 7;
+struct PeerFlags {
+  int* f[MAX_PEERS];
+};
+
+__global__ void peer_signal_kernel(int n, PeerFlags flags, int* counter) {
+  if (threadIdx.x != 0) return;
+  const int v = *counter + 1;
+  *counter = v;
+  __threadfence_system();
+  for (int i = 0; i < n; ++i) asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(flags.f[i]), "r"(v) : "memory");
+}
+
+__global__ void peer_wait_kernel(int n, PeerFlags flags, int* counter, int* bad, unsigned long long timeout_ns) {
+  __shared__ int target;
+  if (threadIdx.x == 0) {
+    target = *counter + 1;
+    *counter = target;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < n) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    int x;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(x) : "l"(flags.f[threadIdx.x]) : "memory");
+      if (x >= target) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {
+        if (bad) atomicOr(bad, 2);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
+inline cudaError_t launch_peer_signal(int n, const PeerFlags& f, int* counter, cudaStream_t st) {
+  peer_signal_kernel<<<1, 32, 0, st>>>(n, f, counter);
+  return cudaGetLastError();
+}
+inline cudaError_t launch_peer_wait(int n, const PeerFlags& f, int* counter, int* bad, unsigned long long timeout_ns,
+                                    cudaStream_t st) {
+  peer_wait_kernel<<<1, 32, 0, st>>>(n, f, counter, bad, timeout_ns);
+  return cudaGetLastError();
+}
+
 }  // namespace ppx

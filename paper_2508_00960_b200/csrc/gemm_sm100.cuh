@@ -55,6 +55,7 @@ constexpr int TMEM_COLS = 512;    // 2 accumulator stages x 256 fp32 columns
 constexpr int MAX_MAPS = 40;
 constexpr int MAX_PROBS = 16;
 constexpr int MAX_SEGS = 8;
+constexpr int MAX_REP = 7;         // peer replicas of an epilogue output (world <= 8)
 constexpr int COLSUM_BYTES = 2 * BN_MAX * 4;     // per-CTA column-sum staging, double-buffered by tile parity
 constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 /*align*/ + 256 /*barriers*/ + COLSUM_BYTES;
 
@@ -109,6 +110,10 @@ struct Epilogue {
   const float* hyper;   // device scalars: [lr, beta1, beta2, eps, bias_corr1, bias_corr2]
   float scale;       // delta scale (1 or 1/B)
   float loss_scale;  // 0.5 or 0.5/B
+  int nrep;          // plain stores only: also write every output element at out + rep_off[r] bytes
+  int pad_rep_;
+  long long rep_off[MAX_REP];   // (peer copies of the output buffer mapped over NVLink: the phantom
+                                // all-gather fused into the compression GEMM's epilogue)
 };
 
 struct Problem {
@@ -663,7 +668,14 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] += (ok(i) && live) ? o[i] : 0.f;
           }
-          if (live) store32(E.out, ooff, nvalid, v);
+          if (live) {
+            store32(E.out, ooff, nvalid, v);
+            for (int r = 0; r < E.nrep; ++r) {
+              Tensor2 t = E.out;
+              t.ptr = reinterpret_cast<char*>(E.out.ptr) + E.rep_off[r];
+              store32(t, ooff, nvalid, v);
+            }
+          }
           if (flags & EP_COLSUM) {
             if (!F) {
 #pragma unroll

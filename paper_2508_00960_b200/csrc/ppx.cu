@@ -32,6 +32,8 @@ struct ppx_ctx {
   // FP32-tier hi/lo split workspace: a pool of chunks, bump-allocated per call and reused by the
   // next call (stream ordered: FP32-tier calls of one ctx must share a stream)
   std::vector<std::pair<char*, size_t>> ws;
+  std::vector<void*> ipc_own;      // ppx_peer_alloc regions (cudaFree at destroy)
+  std::vector<void*> ipc_mapped;   // ppx_peer_open mappings (cudaIpcCloseMemHandle at destroy)
 };
 
 namespace {
@@ -573,6 +575,31 @@ struct Builder {
       }
       if (!changed) break;
     }
+    // wave quantisation: halve the N tiles when the finer grid finishes sooner, modelling a
+    // half-width tile as costing 0.5 / qbal of a full one (PPX_QBAL; 0 disables)
+    {
+      static const double qbal = getenv("PPX_QBAL") ? atof(getenv("PPX_QBAL")) : 0.0;
+      const int C = slots - (use_pair ? ctx->reserved_sms / 2 : ctx->reserved_sms);
+      for (int guard = 0; qbal > 0 && C > 0 && guard < 2; ++guard) {
+        const int T1 = count_tiles();
+        Problem save[ppx::MAX_PROBS];
+        memcpy(save, P.probs, sizeof(Problem) * P.nprobs);
+        bool changed = false;
+        for (int i = 0; i < P.nprobs; ++i) {
+          Problem& pr = P.probs[i];
+          const int gran = use_pair ? (prob_bmn[i] ? 128 : 64) : (prob_bmn[i] ? CH : 32);
+          if (pr.nspan > 1) { pr.nspan = 1; pr.BN /= 2; changed = true; continue; }
+          if (pr.BN / 2 >= gran && (pr.BN / 2) % gran == 0 && (pr.BN / 2) % 16 == 0 && pr.nb_extent > pr.BN / 2) {
+            pr.BN /= 2;
+            pr.npb = (int)cdiv(pr.nb_extent, pr.BN);
+            changed = true;
+          }
+        }
+        const int T2 = count_tiles();
+        const double t1 = (double)((T1 + C - 1) / C), t2 = (double)((T2 + C - 1) / C) * 0.5 / qbal;
+        if (!changed || t2 >= t1) { memcpy(P.probs, save, sizeof(Problem) * P.nprobs); break; }
+      }
+    }
     if (use_pair && !getenv("PPX_NO_TAILSPLIT")) split_tail(ctx->num_sms / 2 - ctx->reserved_sms / 2);
     for (int i = 0; i < P.nprobs && ok(); ++i)
       for (const PendingSeg& ps : pend[i]) finalize(&P.probs[i], ps);
@@ -702,6 +729,8 @@ ppx_status ppx_destroy(ppx_ctx* ctx) {
   if (!ctx) return PPX_OK;
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (auto& c : ctx->ws) cudaFree(c.first);
+  for (void* m : ctx->ipc_mapped) cudaIpcCloseMemHandle(m);
+  for (void* m : ctx->ipc_own) cudaFree(m);
   delete ctx;
   return PPX_OK;
 }
@@ -937,6 +966,77 @@ ppx_status ppx_error_phantoms_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx
     ppx_status st = b.launch();
     if (st != PPX_OK) return st;
   }
+  return PPX_OK;
+}
+
+// ---- NVLink peer memory: the phantom all-gather as NVLink stores from the compression GEMM ----
+ppx_status ppx_peer_alloc(ppx_ctx* ctx, int64_t bytes, void** ptr, uint8_t* handle) {
+  if (!ctx || bytes <= 0 || !ptr || !handle) return PPX_E_CONFIG;
+  void* p = nullptr;
+  CUDA_TRY(ctx, cudaMalloc(&p, (size_t)bytes));
+  ctx->ipc_own.push_back(p);
+  CUDA_TRY(ctx, cudaMemset(p, 0, (size_t)bytes));
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+  CUDA_TRY(ctx, cudaIpcGetMemHandle(&h, p));
+  memcpy(handle, &h, 64);
+  *ptr = p;
+  return PPX_OK;
+}
+
+ppx_status ppx_peer_open(ppx_ctx* ctx, const uint8_t* handle, void** peer_ptr) {
+  if (!ctx || !handle || !peer_ptr) return PPX_E_CONFIG;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, 64);
+  void* p = nullptr;
+  CUDA_TRY(ctx, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  ctx->ipc_mapped.push_back(p);
+  *peer_ptr = p;
+  return PPX_OK;
+}
+
+ppx_status ppx_compress_push(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B,
+                             void* phantoms, int32_t n_peers, void* const* peer_phantoms, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (n < 1 || !io || n_peers < 0 || n_peers > ppx::MAX_REP || (n_peers && !peer_phantoms))
+    return fail(ctx, PPX_E_CONFIG, "ppx_compress_push: bad arguments");
+  Builder b(ctx, dt, stream);
+  for (int i = 0; i < n; ++i) {
+    ppx_status s = add_compress(ctx, dt, b, io[i], B, phantoms);
+    if (s != PPX_OK) return s;
+    Problem& pr = b.P.probs[b.P.nprobs - 1];
+    pr.epi.nrep = n_peers;
+    for (int r = 0; r < n_peers; ++r)
+      pr.epi.rep_off[r] = (long long)((const char*)peer_phantoms[r] - (const char*)phantoms);
+  }
+  return b.launch();
+}
+
+static ppx_status peer_flags(ppx_ctx* ctx, int32_t n, int32_t* const* flags, ppx::PeerFlags& f) {
+  if (n < 0 || n > ppx::MAX_PEERS || (n && !flags)) return fail(ctx, PPX_E_CONFIG, "peer flags: bad arguments");
+  memset(&f, 0, sizeof(f));
+  for (int i = 0; i < n; ++i) f.f[i] = flags[i];
+  return PPX_OK;
+}
+
+ppx_status ppx_peer_signal(ppx_ctx* ctx, int32_t n, int32_t* const* flags, int32_t* counter, void* stream) {
+  if (!ctx || !counter) return PPX_E_CONFIG;
+  ppx::PeerFlags f;
+  ppx_status s = peer_flags(ctx, n, flags, f);
+  if (s != PPX_OK) return s;
+  CUDA_TRY(ctx, ppx::launch_peer_signal(n, f, counter, (cudaStream_t)stream));
+  return PPX_OK;
+}
+
+ppx_status ppx_peer_wait(ppx_ctx* ctx, int32_t n, int32_t* const* flags, int32_t* counter, int32_t* bad,
+                         void* stream) {
+  if (!ctx || !counter) return PPX_E_CONFIG;
+  ppx::PeerFlags f;
+  ppx_status s = peer_flags(ctx, n, flags, f);
+  if (s != PPX_OK) return s;
+  const char* env = getenv("PPX_PEER_TIMEOUT_S");
+  const double secs = env ? atof(env) : 30.0;
+  CUDA_TRY(ctx, ppx::launch_peer_wait(n, f, counter, bad, (unsigned long long)(secs * 1e9), (cudaStream_t)stream));
   return PPX_OK;
 }
 

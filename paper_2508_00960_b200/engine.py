@@ -105,7 +105,15 @@ class PhantomEngine:
         # phantom all-gather buffers; on multi-GPU runs the batch is split in two halves
         # [2][p][B/2, ldk] so each half's all-gather hides behind the other half's GEMMs
         self.halves = 2 if (world > 1 and B % 128 == 0 and os.environ.get("PPX_HALVES", "1") == "2") else 1
-        self.G = [torch.zeros((p, B, ldk), dtype=dtype, device=self.dev) for _ in range(L)]
+        # NVLink phantom exchange (world > 1): the G buffers live in IPC-shared memory; the
+        # compression GEMM stores every phantom tile into all peers' G buffers and a per-layer
+        # flag replaces the NCCL all-gather (PPX_P2P=1; default NCCL)
+        self.p2p = world > 1 and os.environ.get("PPX_P2P", "0") != "0" and self._dist_ready()
+        if self.p2p:
+            self.halves = 1
+            self._setup_p2p(dtype)
+        else:
+            self.G = [torch.zeros((p, B, ldk), dtype=dtype, device=self.dev) for _ in range(L)]
         self.H = [torch.zeros((p, B, ldk), dtype=dtype, device=self.dev) for _ in range(L)]
         self.loss = torch.zeros(1, dtype=f32, device=self.dev)
         self.bad = torch.zeros(1, dtype=torch.int32, device=self.dev)
@@ -125,8 +133,58 @@ class PhantomEngine:
         self._keep = []   # ctypes structs of the launch being built
         self._launches = 0
         self.launch_count = 0
+        self.trace = []   # kernel-launching ABI calls of the last step body (profiling labels)
 
     # ------------------------------------------------------------------------------------------
+    @staticmethod
+    def _dist_ready():
+        import torch.distributed as dist
+        return dist.is_available() and dist.is_initialized()
+
+    def _setup_p2p(self, dtype):
+        """IPC region [L][p, B, ldk] phantoms + [L][world] int32 flags on every GPU, mapped by all
+        peers (handles exchanged over torch.distributed); identical layouts, so a peer address
+        is peer_base + (local address - local base)."""
+        import torch.distributed as dist
+        p, B, L, ldk, world = self.p, self.B, self.L, self.off["ldk"], self.world
+        esz = torch.tensor([], dtype=dtype).element_size()
+        gbytes = p * B * ldk * esz
+        self._goff = [l * gbytes for l in range(L)]
+        self._foff = L * gbytes
+        nbytes = self._foff + ((L * world * 4 + 255) // 256) * 256
+        ptr = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(64)
+        self.ctx.call("ppx_peer_alloc", nbytes, ctypes.byref(ptr), handle)
+        self._pbase = ptr.value
+        handles = [None] * world
+        dist.all_gather_object(handles, handle.raw)
+        self._peer_base = {}
+        for g in range(world):
+            if g != self.rank:
+                q = ctypes.c_void_p()
+                self.ctx.call("ppx_peer_open", handles[g], ctypes.byref(q))
+                self._peer_base[g] = q.value
+        self._peers = [g for g in range(world) if g != self.rank]
+
+        class _Raw:   # torch view of the region (owned by the ctx, freed by ppx_destroy)
+            def __init__(self, addr, n):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": "|u1", "data": (addr, False),
+                                                 "version": 3}
+        raw = torch.as_tensor(_Raw(self._pbase, nbytes), device=self.dev)
+        self.G = [raw[o:o + gbytes].view(dtype).view(p, B, ldk) for o in self._goff]
+        self._sigcnt = torch.zeros(L, dtype=torch.int32, device=self.dev)
+        self._waitcnt = torch.zeros(L, dtype=torch.int32, device=self.dev)
+        n = len(self._peers)
+        mk = lambda addrs: (ctypes.c_void_p * max(n, 1))(*addrs)   # noqa: E731
+        self._push_dst = [mk([self._peer_base[g] + o for g in self._peers]) for o in self._goff]
+        # flag (l, src) lives at foff + 4 (l * world + src) in the region of the GPU that waits
+        self._sig_dst = [mk([self._peer_base[g] + self._foff + 4 * (l * world + self.rank) for g in self._peers])
+                         for l in range(L)]
+        self._wait_src = [mk([self._pbase + self._foff + 4 * (l * world + g) for g in self._peers])
+                          for l in range(L)]
+        torch.cuda.synchronize()
+        dist.barrier()
+
     def _init_weights(self, seed):
         """Glorot-uniform bounds of the reference init (phantom.py:126-129), drawn on device."""
         s, k, p, off = self.s, self.k, self.p, self.off
@@ -221,7 +279,8 @@ class PhantomEngine:
         return self.H[l].data_ptr() + j * self.B * self.off["ldk"] * self.H[l].element_size()
 
     _KERNEL_CALLS = {"ppx_compress", "ppx_forward_update", "ppx_forward_output", "ppx_error_phantoms", "ppx_wgrad",
-                     "ppx_backward_delta", "ppx_optimizer_step", "ppx_compress_n", "ppx_forward_n", "ppx_error_phantoms_n",
+                     "ppx_backward_delta", "ppx_optimizer_step", "ppx_compress_n", "ppx_forward_n", "ppx_error_phantoms_n", "ppx_compress_push",
+                     "ppx_peer_signal", "ppx_peer_wait",
                      "ppx_backward_delta_n"}
 
     def _call(self, name, *args):
@@ -229,6 +288,7 @@ class PhantomEngine:
         self.ctx.call(name, *args)
         if name in self._KERNEL_CALLS:
             self._launches += 1
+            self.trace.append(name)
 
     @staticmethod
     def _join(src: torch.cuda.Stream, dst: torch.cuda.Stream):
@@ -263,6 +323,13 @@ class PhantomEngine:
 
         def compress(l, h):
             ios = [self._io(jj, l, par, x=rows(self.Y[par][jj][l], h), ld_x=s) for jj in range(R)]
+            if self.p2p:   # fused all-gather: NVLink stores from the epilogue, then the layer flag
+                n = len(self._peers)
+                for c in range(0, R, self.group):
+                    self._call("ppx_compress_push", pdt, min(self.group, R - c), self._ios(ios[c:c + self.group]),
+                               Bh, self._gh(l, h), n, self._push_dst[l], st)
+                self._call("ppx_peer_signal", n, self._sig_dst[l], self._sigcnt[l:].data_ptr(), st)
+                return
             for c in range(0, R, self.group):
                 self._call("ppx_compress_n", pdt, min(self.group, R - c), self._ios(ios[c:c + self.group]), Bh,
                            self._gh(l, h), st)
@@ -283,6 +350,9 @@ class PhantomEngine:
             for h in range(H):
                 if (l, h) in ag_done:
                     S.wait_event(ag_done[(l, h)])
+                if self.p2p:
+                    self._call("ppx_peer_wait", len(self._peers), self._wait_src[l], self._waitcnt[l:].data_ptr(),
+                               self.bad.data_ptr(), st)
                 ios = []
                 for jj in range(R):
                     kw = dict(x=rows(self.Y[par][jj][l], h), ld_x=s, out=rows(self.Y[par][jj][l + 1], h), ld_out=s)
@@ -382,6 +452,7 @@ class PhantomEngine:
     def _step_body(self, par, S):
         self._keep.clear()
         self._launches = 0
+        self.trace = []
         c, st = self.ctx, S.cuda_stream
         self._call("ppx_zero", self.gbias.data_ptr(), self.gbias.numel() * 4, st)
         self._call("ppx_zero", self.loss.data_ptr(), 4, st)
@@ -463,6 +534,8 @@ class PhantomEngine:
         self.out_host.copy_(self.loss, non_blocking=True)
         self.bad_host.copy_(self.bad, non_blocking=True)
         torch.cuda.current_stream().synchronize()
+        if int(self.bad_host[0]) & 2:
+            raise TrainingError("a peer GPU never published its phantoms (NVLink exchange timed out)")
         if int(self.bad_host[0]) != 0:
             raise TrainingError("non-finite gradient detected on the device")
         return float(self.out_host[0].item())
