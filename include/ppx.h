@@ -155,7 +155,8 @@ typedef struct {
 /* n x ppx_compress in one launch */
 ppx_status ppx_compress_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B,
                           void* phantoms, void* stream);
-/* n x ppx_forward_update (output_layer = 0) or n x ppx_forward_output (output_layer = 1) */
+/* n x ppx_forward_update (output_layer = 0) or n x ppx_forward_output (output_layer = 1; io.out
+   may then be NULL: the training step needs only the delta, the loss and the bias gradient) */
 ppx_status ppx_forward_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B, ppx_act act,
                          const void* phantoms, int32_t output_layer, float delta_scale, float loss_scale,
                          float* loss, void* stream);
@@ -177,6 +178,11 @@ ppx_status ppx_compress_push(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_ra
 /* *counter += 1, then every flags[i] (an int32 in a peer's region) = *counter (release, system
    scope).  Stream-ordered after the pushes it publishes. */
 ppx_status ppx_peer_signal(ppx_ctx* ctx, int32_t n, int32_t* const* flags, int32_t* counter, void* stream);
+/* The phantom all-gather as one NVLink kernel: copies `bytes` (multiple of 16) at src to dsts[i]
+   (peer mappings, same offsets) with 16-byte posted stores, then — once every CTA has fenced —
+   *counter += 1 and every flags[i] = *counter (release, system scope).  Pairs with ppx_peer_wait. */
+ppx_status ppx_peer_push(ppx_ctx* ctx, const void* src, int64_t bytes, int32_t n, void* const* dsts,
+                         int32_t* const* flags, int32_t* counter, void* stream);
 /* *counter += 1, then wait until every flags[i] (local int32s written by the peers) >= *counter
    (acquire, system scope).  After PPX_PEER_TIMEOUT_S seconds (default 30) it sets bit 1 of *bad
    and returns instead of hanging. */
@@ -207,6 +213,12 @@ ppx_status ppx_error_phantoms_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx
    it, slot j of `contrib` (for this GPU's local ranks) is the sum over all GPUs. */
 ppx_status ppx_reduce_scatter(ppx_ctx* ctx, ppx_dtype dt, void* contrib, int64_t slot_elems,
                               int32_t local_ranks, void* stream);
+
+/* out-of-place reduce-scatter: recv [local_ranks, slot] = this GPU's slots of the sum over GPUs of
+   contrib [p, slot] (collectives.py:122-127, 345-357); contrib is not modified, so slots no
+   local rank writes (the own slot when one logical rank per GPU) stay zero across steps. */
+ppx_status ppx_reduce_scatter_to(ppx_ctx* ctx, ppx_dtype dt, const void* contrib, void* recv,
+                                 int64_t slot_elems, int32_t local_ranks, void* stream);
 
 /* collectives.py:138-142 — elementwise fp32 sum over GPUs, in place (the scalar loss,
    training.py:70). */

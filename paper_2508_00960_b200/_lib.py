@@ -86,9 +86,11 @@ _SIGS = {
                                 _vp, _i64, _f32, _f32, _fp, _vp]),
     "ppx_error_phantoms": (_i32, [_vp, _i32, ctypes.POINTER(Layer), _i32, _vp, _i64, _vp, _i32, _vp]),
     "ppx_error_phantoms_n": (_i32, [_vp, _i32, _i32, ctypes.POINTER(RankIO), _i32, _vp, _vp]),
+    "ppx_reduce_scatter_to": (_i32, [_vp, _i32, _vp, _vp, _i64, _i32, _vp]),
     "ppx_peer_alloc": (_i32, [_vp, _i64, ctypes.POINTER(_vp), ctypes.c_char_p]),
     "ppx_peer_open": (_i32, [_vp, ctypes.c_char_p, ctypes.POINTER(_vp)]),
     "ppx_compress_push": (_i32, [_vp, _i32, _i32, ctypes.POINTER(RankIO), _i32, _vp, _i32, ctypes.POINTER(_vp), _vp]),
+    "ppx_peer_push": (_i32, [_vp, _vp, _i64, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp]),
     "ppx_peer_signal": (_i32, [_vp, _i32, ctypes.POINTER(_vp), _vp, _vp]),
     "ppx_peer_wait": (_i32, [_vp, _i32, ctypes.POINTER(_vp), _vp, _vp, _vp]),
     "ppx_reduce_scatter": (_i32, [_vp, _i32, _vp, _i64, _i32, _vp]),

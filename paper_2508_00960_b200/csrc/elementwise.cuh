@@ -250,6 +250,42 @@ __global__ void peer_wait_kernel(int n, PeerFlags flags, int* counter, int* bad,
   __threadfence_system();
 }
 
+// The phantom all-gather as ONE kernel over NVLink: every CTA copies a strided share of this
+// GPU's phantom chunk (16-byte vectors, read once from local HBM) into the same offset of every
+// peer's buffer (posted NVLink stores), then fences at system scope; the last CTA to finish
+// publishes the new counter value into every peer's flag (release) — peer_wait_kernel consumes it.
+struct PeerPtrs {
+  char* p[MAX_PEERS];
+};
+__global__ void peer_push_kernel(const uint4* __restrict__ src, long long n16, int n, PeerPtrs dst, PeerFlags flags,
+                                 int* counter, unsigned int* arrive) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) {
+    const uint4 v = src[i];
+#pragma unroll 1
+    for (int r = 0; r < n; ++r) reinterpret_cast<uint4*>(dst.p[r])[i] = v;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(arrive, 1u);
+    if (prev == gridDim.x - 1) {
+      *arrive = 0u;
+      const int v = *counter + 1;
+      *counter = v;
+      __threadfence_system();
+      for (int r = 0; r < n; ++r)
+        asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(flags.f[r]), "r"(v) : "memory");
+    }
+  }
+}
+inline cudaError_t launch_peer_push(const void* src, long long bytes, int n, const PeerPtrs& dst, const PeerFlags& f,
+                                    int* counter, unsigned int* arrive, int blocks, cudaStream_t st) {
+  peer_push_kernel<<<blocks, 512, 0, st>>>(reinterpret_cast<const uint4*>(src), bytes / 16, n, dst, f, counter,
+                                           arrive);
+  return cudaGetLastError();
+}
+
 inline cudaError_t launch_peer_signal(int n, const PeerFlags& f, int* counter, cudaStream_t st) {
   peer_signal_kernel<<<1, 32, 0, st>>>(n, f, counter);
   return cudaGetLastError();

@@ -125,6 +125,11 @@ struct Problem {
   int m_base;        // first row covered by this problem's tiles (a split-off tail of a problem)
   int nspan;         // 2-SM kernel: N blocks per tile (2 = each CTA of the pair owns one whole N block)
   int tile_begin;    // prefix over problems
+  int ksplit;        // 2-SM kernel: 2 = K split in two halves; tiles [0, split_tiles) run the first
+  int kst_total;     //   half (stages [0, kst_total/2) over all segments) and park fp32 partials in
+  int split_tiles;   //   `part`, the second half's tiles add them and run the epilogue
+  float* part;       // [split_tiles][2 CTAs][128 rows][BN] fp32
+  int* pflag;        // [split_tiles][2]: 1 = partial ready (set by half 0, cleared by half 1)
   int nsegs;
   Segment segs[MAX_SEGS];
   Epilogue epi;
@@ -481,6 +486,7 @@ __device__ __forceinline__ float warp_transpose_sum(float* v, int lane) {
 // ------------------------------------------------------------------------------------------
 struct TileCoord {
   int prob, m0, qn, nin;
+  int split, tin;    // K half of a split problem and the tile's index inside its half
 };
 
 template <int MT>
@@ -490,6 +496,11 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, int t) {
   while (pi + 1 < P.nprobs && t >= P.probs[pi + 1].tile_begin) ++pi;
   const Problem& pr = P.probs[pi];
   int local = t - pr.tile_begin;
+  int split = 0;
+  if (pr.ksplit > 1 && local >= pr.split_tiles) {
+    split = 1;
+    local -= pr.split_tiles;
+  }
   const int span = pr.nspan > 1 ? pr.nspan : 1;
   int ntn = (pr.nblk + span - 1) / span * pr.npb;
   int mt = local / ntn;
@@ -499,6 +510,8 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, int t) {
   c.m0 = pr.m_base + mt * MT;
   c.qn = nt / pr.npb * span;
   c.nin = (nt - c.qn * pr.npb) * pr.BN;
+  c.split = split;
+  c.tin = local;
   return c;
 }
 
@@ -532,7 +545,13 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
     rows_valid = rows_valid < 0 ? 0 : (rows_valid > 32 ? 32 : rows_valid);
     const int row = row0 + lane;
     const bool row_ok = lane < rows_valid;
-    const uint32_t flags = E.flags;
+    // split-K: the first half only parks its raw accumulators; the second half adds them first
+    const bool sp0 = pr.ksplit > 1 && tc.split == 0;
+    const bool sp1 = pr.ksplit > 1 && tc.split == 1;
+    float* const part = pr.ksplit > 1 ? pr.part + ((size_t)(tc.tin * 2 + (int)crank) * BM + wq * 32 + lane) * pr.BN
+                                      : nullptr;
+    int* const pflag = pr.ksplit > 1 ? pr.pflag + tc.tin * 2 + (int)crank : nullptr;
+    const uint32_t flags = sp0 ? 0u : E.flags;
     const bool upd = (flags & (EP_SGD | EP_ADAM)) != 0;
     // per-row input streamed one chunk ahead: target | fp32 master | ReLU mask | accumulated output
     const Tensor2* sa = (flags & EP_LOSS) ? &E.target
@@ -571,6 +590,12 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
     mbar_wait_t(tfull_bar(as), aphase, kStats && P.stats != nullptr, st_wait);
     const unsigned long long c_busy = kStats && P.stats ? clock64() : 0ull;
     tc_fence_after();
+    if (sp1) {   // the partner tile (lower index, so scheduled no later) publishes its partial
+      int x;
+      do {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(x) : "l"(pflag) : "memory");
+      } while (x == 0);
+    }
     float loss_acc = 0.f;
     bool bad = false;
     Pre32 pa;
@@ -599,6 +624,24 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
       const unsigned long long c_t0 = kStats && P.stats ? clock64() : 0ull;
       tmem_ld32(tmem_base + as * BN_MAX + c * 32 + ((uint32_t)(wq * 32) << 16), v);
       if (kStats && P.stats) st_tmem += clock64() - c_t0;
+      if (sp0) {
+        float4* q = reinterpret_cast<float4*>(part + c * 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) q[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        pa = na;
+        continue;
+      }
+      if (sp1) {
+        const float4* q = reinterpret_cast<const float4*>(part + c * 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 w4 = q[i];
+          v[4 * i] += w4.x;
+          v[4 * i + 1] += w4.y;
+          v[4 * i + 2] += w4.z;
+          v[4 * i + 3] += w4.w;
+        }
+      }
       // full chunks (every row and column valid, the common case) compile without per-element masks
       auto body = [&](auto full_c) {
         constexpr bool F = decltype(full_c)::value;
@@ -643,7 +686,7 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
             v[i] = y;
           }
           if (live) {
-            store32(E.out, ooff, nvalid, v);
+            if (E.out.ptr) store32(E.out, ooff, nvalid, v);
             store32(E.aux, (long long)row * E.aux.ld + col0, nvalid, tg);
           }
           if (flags & EP_COLSUM) {
@@ -708,6 +751,17 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
         for (int j = lane; j < pr.BN; j += 32) {
           if (j < ncols) atomicAdd(E.colsum + tc.nin + j, cb[j]);
           cb[j] = 0.f;
+        }
+      }
+    }
+    if (pr.ksplit > 1) {   // all epilogue warps of this CTA are done with the partial
+      asm volatile("bar.sync 2, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
+      if (warp == 0 && lane == 0) {
+        if (sp0) {
+          __threadfence();
+          asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(pflag), "r"(1) : "memory");
+        } else {
+          asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(pflag), "r"(0) : "memory");
         }
       }
     }

@@ -34,6 +34,13 @@ struct ppx_ctx {
   std::vector<std::pair<char*, size_t>> ws;
   std::vector<void*> ipc_own;      // ppx_peer_alloc regions (cudaFree at destroy)
   std::vector<void*> ipc_mapped;   // ppx_peer_open mappings (cudaIpcCloseMemHandle at destroy)
+  // split-K partials and ready flags of the 2-SM kernel (flags self-reset: one split launch in
+  // flight per ctx, i.e. split GEMMs of one ctx must share a stream)
+  float* sk_part = nullptr;
+  size_t sk_part_cap = 0;
+  int* sk_flag = nullptr;
+  size_t sk_flag_cap = 0;
+  unsigned int* push_arrive = nullptr;   // ppx_peer_push's CTA arrival counter (self-resetting)
 };
 
 namespace {
@@ -483,7 +490,79 @@ struct Builder {
 
   static int ptiles(const Problem& pr) {
     const int span = pr.nspan > 1 ? pr.nspan : 1;
-    return pr.m_tiles * (int)cdiv(pr.nblk, span) * pr.npb;
+    return pr.m_tiles * (int)cdiv(pr.nblk, span) * pr.npb * (pr.ksplit > 1 ? 2 : 1);
+  }
+
+  // Split-K for launches too small to fill the GPU (e.g. one logical rank's weight gradients:
+  // ~100 long tiles on 74 clusters = 2 rounds, the second 40% full): when a simulation of the
+  // static round-robin schedule says halving every long problem's K finishes >10% sooner, each
+  // such problem runs its tiles twice (first / second K half); the second half adds the first
+  // half's fp32 partial and runs the real epilogue.
+  bool choose_ksplit(int C) {
+    // measured on B200 (one logical rank's weight gradients, 104 tiles): the extra tile
+    // prologues / exposed epilogues outweigh the better rounds, so it is opt-in (PPX_SPLITK=1)
+    if (C < 1 || !getenv("PPX_SPLITK") || getenv("PPX_NO_SPLITK")) return false;
+    int kst[ppx::MAX_PROBS], bt[ppx::MAX_PROBS];
+    for (int i = 0; i < P.nprobs; ++i) {
+      kst[i] = 0;
+      for (const PendingSeg& ps : pend[i]) kst[i] += (int)cdiv(ps.kext, ppx::PBK) * ps.nkblk;
+      bt[i] = ptiles(P.probs[i]);
+    }
+    auto sim = [&](bool sp) {
+      std::vector<double> load(C, 0.0);
+      int t = 0;
+      for (int i = 0; i < P.nprobs; ++i) {
+        const bool el = sp && kst[i] >= 16;
+        for (int h = 0; h < (el ? 2 : 1); ++h) {
+          const double cost = el ? kst[i] / 2.0 + 6.0 : kst[i] + 4.0;
+          for (int j = 0; j < bt[i]; ++j) load[t++ % C] += cost;
+        }
+      }
+      double m = 0;
+      for (double x : load) m = x > m ? x : m;
+      return m;
+    };
+    if (sim(true) >= 0.9 * sim(false)) return false;
+    size_t nf = 0, np = 0;
+    for (int i = 0; i < P.nprobs; ++i)
+      if (kst[i] >= 16) {
+        nf += 2 * (size_t)bt[i];
+        np += 2 * (size_t)bt[i] * ppx::BM * P.probs[i].BN;
+      }
+    if (np > ctx->sk_part_cap || nf > ctx->sk_flag_cap) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+      cudaDeviceSynchronize();
+      if (np > ctx->sk_part_cap) {
+        if (ctx->sk_part) cudaFree(ctx->sk_part);
+        ctx->sk_part = nullptr;
+        ctx->sk_part_cap = 0;
+        if (cudaMalloc(&ctx->sk_part, np * sizeof(float)) != cudaSuccess) { ctx->sk_part = nullptr; return false; }
+        ctx->sk_part_cap = np;
+      }
+      if (nf > ctx->sk_flag_cap) {
+        if (ctx->sk_flag) cudaFree(ctx->sk_flag);
+  if (ctx->push_arrive) cudaFree(ctx->push_arrive);
+        ctx->sk_flag = nullptr;
+        ctx->sk_flag_cap = 0;
+        if (cudaMalloc(&ctx->sk_flag, nf * sizeof(int)) != cudaSuccess) { ctx->sk_flag = nullptr; return false; }
+        if (cudaMemset(ctx->sk_flag, 0, nf * sizeof(int)) != cudaSuccess) return false;
+        ctx->sk_flag_cap = nf;
+      }
+    }
+    size_t fo = 0, po = 0;
+    for (int i = 0; i < P.nprobs; ++i) {
+      Problem& pr = P.probs[i];
+      if (kst[i] < 16) continue;
+      pr.ksplit = 2;
+      pr.kst_total = kst[i];
+      pr.split_tiles = bt[i];
+      pr.part = ctx->sk_part + po;
+      pr.pflag = ctx->sk_flag + fo;
+      po += 2 * (size_t)bt[i] * ppx::BM * pr.BN;
+      fo += 2 * (size_t)bt[i];
+    }
+    return true;
   }
 
   // 2-SM kernel: a problem whose N blocks (slots) are each at most half a tile wide runs tiles
@@ -600,7 +679,8 @@ struct Builder {
         if (!changed || t2 >= t1) { memcpy(P.probs, save, sizeof(Problem) * P.nprobs); break; }
       }
     }
-    if (use_pair && !getenv("PPX_NO_TAILSPLIT")) split_tail(ctx->num_sms / 2 - ctx->reserved_sms / 2);
+    const bool ksplit = use_pair && choose_ksplit(ctx->num_sms / 2 - ctx->reserved_sms / 2);
+    if (use_pair && !ksplit && !getenv("PPX_NO_TAILSPLIT")) split_tail(ctx->num_sms / 2 - ctx->reserved_sms / 2);
     for (int i = 0; i < P.nprobs && ok(); ++i)
       for (const PendingSeg& ps : pend[i]) finalize(&P.probs[i], ps);
     if (!ok()) return status;
@@ -730,6 +810,9 @@ ppx_status ppx_destroy(ppx_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (auto& c : ctx->ws) cudaFree(c.first);
   for (void* m : ctx->ipc_mapped) cudaIpcCloseMemHandle(m);
+  if (ctx->sk_part) cudaFree(ctx->sk_part);
+  if (ctx->sk_flag) cudaFree(ctx->sk_flag);
+  if (ctx->push_arrive) cudaFree(ctx->push_arrive);
   for (void* m : ctx->ipc_own) cudaFree(m);
   delete ctx;
   return PPX_OK;
@@ -795,7 +878,9 @@ static ppx_status add_forward(ppx_ctx* ctx, ppx_dtype dt, Builder& b, const ppx_
                               const void* phantoms, int output_layer, float delta_scale, float loss_scale,
                               float* loss) {
   const ppx_layer* L = io.layer;
-  if (bad_layer(L) || B < 1 || !io.x || !io.out) return fail(ctx, PPX_E_CONFIG, "forward: bad arguments");
+  // the output layer may skip storing y (training needs only the delta and the loss)
+  if (bad_layer(L) || B < 1 || !io.x || (!io.out && !output_layer))
+    return fail(ctx, PPX_E_CONFIG, "forward: bad arguments");
   if (output_layer && (!io.target || !io.aux || !loss)) return fail(ctx, PPX_E_CONFIG, "forward output: bad arguments");
   Flat f(L->s, L->k, L->p);
   Problem* pr = b.new_problem(B, L->s, 1, false);
@@ -972,6 +1057,10 @@ ppx_status ppx_error_phantoms_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx
 // ---- NVLink peer memory: the phantom all-gather as NVLink stores from the compression GEMM ----
 ppx_status ppx_peer_alloc(ppx_ctx* ctx, int64_t bytes, void** ptr, uint8_t* handle) {
   if (!ctx || bytes <= 0 || !ptr || !handle) return PPX_E_CONFIG;
+  if (!ctx->push_arrive) {   // ppx_peer_push's arrival counter (allocated here: never during capture)
+    CUDA_TRY(ctx, cudaMalloc(&ctx->push_arrive, sizeof(unsigned int)));
+    CUDA_TRY(ctx, cudaMemset(ctx->push_arrive, 0, sizeof(unsigned int)));
+  }
   void* p = nullptr;
   CUDA_TRY(ctx, cudaMalloc(&p, (size_t)bytes));
   ctx->ipc_own.push_back(p);
@@ -1028,6 +1117,25 @@ ppx_status ppx_peer_signal(ppx_ctx* ctx, int32_t n, int32_t* const* flags, int32
   return PPX_OK;
 }
 
+ppx_status ppx_peer_push(ppx_ctx* ctx, const void* src, int64_t bytes, int32_t n, void* const* dsts,
+                         int32_t* const* flags, int32_t* counter, void* stream) {
+  if (!ctx || !src || !counter || bytes < 0 || bytes % 16 || n < 0 || n > ppx::MAX_PEERS || (n && !dsts))
+    return fail(ctx, PPX_E_CONFIG, "ppx_peer_push: bad arguments (bytes must be a multiple of 16)");
+  ppx::PeerFlags f;
+  ppx_status s = peer_flags(ctx, n, flags, f);
+  if (s != PPX_OK) return s;
+  ppx::PeerPtrs d;
+  memset(&d, 0, sizeof(d));
+  for (int i = 0; i < n; ++i) d.p[i] = (char*)dsts[i];
+  if (!ctx->push_arrive) return fail(ctx, PPX_E_SEQUENCING, "ppx_peer_push before ppx_peer_alloc");
+  const char* env = getenv("PPX_PUSH_BLOCKS");
+  int blocks = env ? atoi(env) : 64;
+  const long long need = (bytes / 16 + 511) / 512;
+  if (need < blocks) blocks = need > 0 ? (int)need : 1;
+  CUDA_TRY(ctx, ppx::launch_peer_push(src, bytes, n, d, f, counter, ctx->push_arrive, blocks, (cudaStream_t)stream));
+  return PPX_OK;
+}
+
 ppx_status ppx_peer_wait(ppx_ctx* ctx, int32_t n, int32_t* const* flags, int32_t* counter, int32_t* bad,
                          void* stream) {
   if (!ctx || !counter) return PPX_E_CONFIG;
@@ -1063,6 +1171,19 @@ ppx_status ppx_reduce_scatter(ppx_ctx* ctx, ppx_dtype dt, void* contrib, int64_t
   const int es = dt == PPX_FP32 ? 4 : 2;
   NCCL_TRY(ctx, ncclReduceScatter(base, base + (int64_t)ctx->rank * chunk * es, (size_t)chunk, nccl_type(dt), ncclSum,
                                   ctx->comm, (cudaStream_t)stream));
+  return PPX_OK;
+}
+
+ppx_status ppx_reduce_scatter_to(ppx_ctx* ctx, ppx_dtype dt, const void* contrib, void* recv, int64_t slot_elems,
+                                 int32_t local_ranks, void* stream) {
+  if (!ctx || !contrib || !recv) return PPX_E_CONFIG;
+  const int64_t chunk = slot_elems * local_ranks;
+  const int es = dt == PPX_FP32 ? 4 : 2;
+  if (ctx->world == 1) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(recv, contrib, (size_t)(chunk * es), cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return PPX_OK;
+  }
+  NCCL_TRY(ctx, ncclReduceScatter(contrib, recv, (size_t)chunk, nccl_type(dt), ncclSum, ctx->comm, (cudaStream_t)stream));
   return PPX_OK;
 }
 

@@ -108,13 +108,15 @@ class PhantomEngine:
         # NVLink phantom exchange (world > 1): the G buffers live in IPC-shared memory; the
         # compression GEMM stores every phantom tile into all peers' G buffers and a per-layer
         # flag replaces the NCCL all-gather (PPX_P2P=1; default NCCL)
-        self.p2p = world > 1 and os.environ.get("PPX_P2P", "0") != "0" and self._dist_ready()
+        self.p2p = int(os.environ.get("PPX_P2P", "0")) if world > 1 and self._dist_ready() else 0
         if self.p2p:
             self.halves = 1
             self._setup_p2p(dtype)
         else:
             self.G = [torch.zeros((p, B, ldk), dtype=dtype, device=self.dev) for _ in range(L)]
         self.H = [torch.zeros((p, B, ldk), dtype=dtype, device=self.dev) for _ in range(L)]
+        # out-of-place reduce-scatter target (world > 1): this GPU's R received slots
+        self.Hr = [torch.zeros((R, B, ldk), dtype=dtype, device=self.dev) for _ in range(L)] if world > 1 else None
         self.loss = torch.zeros(1, dtype=f32, device=self.dev)
         self.bad = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.hyper = torch.zeros(6, dtype=f32, device=self.dev)
@@ -130,6 +132,11 @@ class PhantomEngine:
         self.group = 1 if os.environ.get("PPX_NOGROUP") else R
         self.graphs = [None, None]
         self.parity = 0
+        # training steps skip the output layer's y store (PPX_STORE_OUTPUT=1 keeps it)
+        self.skip_output = not os.environ.get("PPX_STORE_OUTPUT")
+        # timing experiments ONLY (wrong results): drop the backward reduce-scatter
+        self._dbg_skip_rs = bool(os.environ.get("PPX_DEBUG_SKIP_RS"))
+        self._dbg_skip_ag = bool(os.environ.get("PPX_DEBUG_SKIP_AG"))
         self._keep = []   # ctypes structs of the launch being built
         self._launches = 0
         self.launch_count = 0
@@ -276,11 +283,14 @@ class PhantomEngine:
         return u
 
     def _received(self, l, j):
+        if self.Hr is not None:
+            jj = self.local.index(j)
+            return self.Hr[l].data_ptr() + jj * self.B * self.off["ldk"] * self.Hr[l].element_size()
         return self.H[l].data_ptr() + j * self.B * self.off["ldk"] * self.H[l].element_size()
 
     _KERNEL_CALLS = {"ppx_compress", "ppx_forward_update", "ppx_forward_output", "ppx_error_phantoms", "ppx_wgrad",
                      "ppx_backward_delta", "ppx_optimizer_step", "ppx_compress_n", "ppx_forward_n", "ppx_error_phantoms_n", "ppx_compress_push",
-                     "ppx_peer_signal", "ppx_peer_wait",
+                     "ppx_peer_signal", "ppx_peer_wait", "ppx_peer_push",
                      "ppx_backward_delta_n"}
 
     def _call(self, name, *args):
@@ -323,6 +333,18 @@ class PhantomEngine:
 
         def compress(l, h):
             ios = [self._io(jj, l, par, x=rows(self.Y[par][jj][l], h), ld_x=s) for jj in range(R)]
+            if self.p2p == 2:   # compress, then ONE NVLink push kernel (copy to peers + flag)
+                n = len(self._peers)
+                for c in range(0, R, self.group):
+                    self._call("ppx_compress_n", pdt, min(self.group, R - c), self._ios(ios[c:c + self.group]), Bh,
+                               self._gh(l, h), st)
+                own = self._gh(l, h) + self.rank * R * Bh * self.off["ldk"] * esz
+                nbytes = R * Bh * self.off["ldk"] * esz
+                off = own - self._pbase
+                dst = (ctypes.c_void_p * max(n, 1))(*[self._peer_base[g] + off for g in self._peers])
+                self._keep.append(dst)
+                self._call("ppx_peer_push", own, nbytes, n, dst, self._sig_dst[l], self._sigcnt[l:].data_ptr(), st)
+                return
             if self.p2p:   # fused all-gather: NVLink stores from the epilogue, then the layer flag
                 n = len(self._peers)
                 for c in range(0, R, self.group):
@@ -333,7 +355,7 @@ class PhantomEngine:
             for c in range(0, R, self.group):
                 self._call("ppx_compress_n", pdt, min(self.group, R - c), self._ios(ios[c:c + self.group]), Bh,
                            self._gh(l, h), st)
-            if self.world > 1:
+            if self.world > 1 and not self._dbg_skip_ag:
                 self._join(S, self.comm_stream)
                 self._call("ppx_all_gather", pdt, self._gh(l, h), Bh * self.off["ldk"], R,
                            self.comm_stream.cuda_stream)
@@ -356,9 +378,9 @@ class PhantomEngine:
                 ios = []
                 for jj in range(R):
                     kw = dict(x=rows(self.Y[par][jj][l], h), ld_x=s, out=rows(self.Y[par][jj][l + 1], h), ld_out=s)
-                    if last:
-                        kw.update(aux=rows(self.D[jj][0], h), ld_aux=s, target=rows(self.Tgt[par][jj], h), ld_t=s,
-                                  colsum=self.gbias[jj, l].data_ptr())
+                    if last:   # the output y itself is never read by the backward pass: not stored
+                        kw.update(out=None if self.skip_output else kw["out"], aux=rows(self.D[jj][0], h), ld_aux=s,
+                                  target=rows(self.Tgt[par][jj], h), ld_t=s, colsum=self.gbias[jj, l].data_ptr())
                     ios.append(self._io(jj, l, par, **kw))
                 for c in range(0, R, self.group):
                     self._call("ppx_forward_n", pdt, min(self.group, R - c), self._ios(ios[c:c + self.group]), Bh,
@@ -380,10 +402,8 @@ class PhantomEngine:
         for l in range(L - 1, -1, -1):
             if self.group >= R and not os.environ.get("PPX_K3_PERRANK"):
                 # one launch: slot i = sum_{local j != i} delta_j . D_{i->j}, every slot with a
-                # contributor overwritten; with R = 1 the own slot has none and still holds the
-                # previous step's in-place reduce-scatter result, so it is zeroed first
-                if R == 1 and self.world > 1:
-                    self._call("ppx_zero", self._received(l, self.local[0]), slot * esz, st)
+                # contributor overwritten (with R = 1 the own slot has none and stays zero: the
+                # reduce-scatter is out of place)
                 ios = [self._io(jj, l, par, x=self.D[jj][cur].data_ptr(), ld_x=s) for jj in range(R)]
                 self._call("ppx_error_phantoms_n", pdt, R, self._ios(ios), B, self.H[l].data_ptr(), st)
             else:   # PPX_NOGROUP profiling: per-rank launches accumulating into zeroed slots
@@ -391,9 +411,10 @@ class PhantomEngine:
                 for jj in range(R):
                     self._call("ppx_error_phantoms", pdt, ctypes.byref(self._layer(jj, l, par)), B,
                                self.D[jj][cur].data_ptr(), s, self.H[l].data_ptr(), 1, st)
-            if self.world > 1:
+            if self.world > 1 and not self._dbg_skip_rs:
                 self._join(S, self.comm_stream)
-                self._call("ppx_reduce_scatter", pdt, self.H[l].data_ptr(), slot, R, self.comm_stream.cuda_stream)
+                self._call("ppx_reduce_scatter_to", pdt, self.H[l].data_ptr(), self.Hr[l].data_ptr(), slot, R,
+                           self.comm_stream.cuda_stream)
             # weight gradients that do not need r_l, overlapped with the reduce-scatter
             per_rank = []
             for jj in range(R):

@@ -10,8 +10,9 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+@pytest.mark.parametrize("p2p", ["0", "1", "2"])
 @pytest.mark.parametrize("dtype,p", [("fp32", 4), ("bf16", 4), ("fp32", 2), ("bf16", 2)])
-def test_engine_two_gpus_matches_oracle(dtype, p):
+def test_engine_two_gpus_matches_oracle(dtype, p, p2p):
     """p = 4: two logical ranks per GPU; p = 2: one per GPU (the own reduce-scatter slot must be
     re-zeroed every step: the in-place reduce-scatter leaves r_j there)."""
     if torch.cuda.device_count() < 2:
@@ -19,6 +20,7 @@ def test_engine_two_gpus_matches_oracle(dtype, p):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "tools", "mp_parity.py"),
            "--dtype", dtype, "--p", str(p)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    env = dict(os.environ, PPX_P2P=p2p)   # 1: epilogue NVLink stores + flag, 2: NVLink push kernel
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert '"pass": true' in r.stdout
