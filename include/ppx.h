@@ -97,6 +97,8 @@ typedef struct {
 
 /* ---- context / communicator (collectives.py:87-194 Communicator -> NCCL over NVLink) ---- */
 int ppx_abi_version(void);
+/* debugging: the calling thread's pending CUDA runtime error (cudaPeekAtLastError), 0 = none */
+int32_t ppx_peek_error(void);
 int64_t ppx_layer_elems(int32_t s, int32_t k, int32_t p);
 ppx_status ppx_get_unique_id(uint8_t uid[128]);
 /* world GPUs, this process drives GPU `rank` on CUDA device `device`; uid from rank 0
@@ -178,6 +180,23 @@ ppx_status ppx_compress_push(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_ra
 /* *counter += 1, then every flags[i] (an int32 in a peer's region) = *counter (release, system
    scope).  Stream-ordered after the pushes it publishes. */
 ppx_status ppx_peer_signal(ppx_ctx* ctx, int32_t n, int32_t* const* flags, int32_t* counter, void* stream);
+/* Fused compression + phantom all-gather + forward of one layer for the n local ranks, ONE
+   launch of the 2-SM kernel (bf16): the compression tiles store their phantoms into `phantoms`
+   and into every peer's copy (NVLink), then add 1 to every arrive[i] (own counter first); the
+   forward tiles (io as for ppx_forward_n) compute the local block, wait in-kernel until
+   *wait_counter reached this launch's epoch target (all GPUs' compression tiles), then add the
+   decompressed phantoms.  *epoch (per layer, local) is bumped by the launch itself.  Counters
+   start at 0 on every GPU; every GPU must issue the same fused launches in the same order. */
+typedef struct {
+  int32_t n_peers;
+  void* const* peer_phantoms;    /* [n_peers] peer mappings of `phantoms` (same layout) */
+  int32_t* const* arrive;        /* [n_peers + 1] arrival counters of this layer: own, then peers' */
+  const int32_t* wait_counter;   /* this GPU's arrival counter of the layer (== arrive[0]) */
+  int32_t* epoch;                /* this GPU's launch counter of the layer */
+} ppx_exchange;
+ppx_status ppx_forward_fused(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B, ppx_act act,
+                             void* phantoms, int32_t output_layer, float delta_scale, float loss_scale,
+                             float* loss, const ppx_exchange* ex, void* stream);
 /* The phantom all-gather as one NVLink kernel: copies `bytes` (multiple of 16) at src to dsts[i]
    (peer mappings, same offsets) with 16-byte posted stores, then — once every CTA has fenced —
    *counter += 1 and every flags[i] = *counter (release, system scope).  Pairs with ppx_peer_wait. */

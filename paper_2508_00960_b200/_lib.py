@@ -47,6 +47,12 @@ class WgradItem(ctypes.Structure):
                 ("upd", ctypes.POINTER(Update)), ("phantom_halves", _i32)]
 
 
+class Exchange(ctypes.Structure):
+    """ppx_exchange: NVLink peers and counters of one layer's fused forward launch."""
+    _fields_ = [("n_peers", _i32), ("peer_phantoms", ctypes.POINTER(_vp)), ("arrive", ctypes.POINTER(_vp)),
+                ("wait_counter", _vp), ("epoch", _vp)]
+
+
 class RankIO(ctypes.Structure):
     """ppx_rank_io: one logical rank's operands in a grouped launch."""
     _fields_ = [("layer", ctypes.POINTER(Layer)), ("x", _vp), ("ld_x", _i64), ("out", _vp), ("ld_out", _i64),
@@ -87,9 +93,12 @@ _SIGS = {
     "ppx_error_phantoms": (_i32, [_vp, _i32, ctypes.POINTER(Layer), _i32, _vp, _i64, _vp, _i32, _vp]),
     "ppx_error_phantoms_n": (_i32, [_vp, _i32, _i32, ctypes.POINTER(RankIO), _i32, _vp, _vp]),
     "ppx_reduce_scatter_to": (_i32, [_vp, _i32, _vp, _vp, _i64, _i32, _vp]),
+    "ppx_peek_error": (_i32, []),
     "ppx_peer_alloc": (_i32, [_vp, _i64, ctypes.POINTER(_vp), ctypes.c_char_p]),
     "ppx_peer_open": (_i32, [_vp, ctypes.c_char_p, ctypes.POINTER(_vp)]),
     "ppx_compress_push": (_i32, [_vp, _i32, _i32, ctypes.POINTER(RankIO), _i32, _vp, _i32, ctypes.POINTER(_vp), _vp]),
+    "ppx_forward_fused": (_i32, [_vp, _i32, _i32, ctypes.POINTER(RankIO), _i32, _i32, _vp, _i32, _f32, _f32, _fp,
+                                   ctypes.POINTER(Exchange), _vp]),
     "ppx_peer_push": (_i32, [_vp, _vp, _i64, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp]),
     "ppx_peer_signal": (_i32, [_vp, _i32, ctypes.POINTER(_vp), _vp, _vp]),
     "ppx_peer_wait": (_i32, [_vp, _i32, ctypes.POINTER(_vp), _vp, _vp, _vp]),
@@ -117,6 +126,7 @@ EXPORTS = tuple(_SIGS)
 
 _lib = None
 _lock = threading.Lock()
+_DEBUG_ERRORS = bool(os.environ.get("PPX_DEBUG_ERRORS"))
 
 
 def load():
@@ -177,6 +187,10 @@ class Context:
 
     def call(self, name: str, *args):
         check(getattr(load(), name)(self.handle, *args), self.handle, name)
+        if _DEBUG_ERRORS:
+            e = load().ppx_peek_error()
+            if e:
+                raise DeviceError(f"{name} left CUDA runtime error {e} pending")
 
     @property
     def num_sms(self) -> int:

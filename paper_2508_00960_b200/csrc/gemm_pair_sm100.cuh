@@ -98,6 +98,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot_ptr;
+  // programmatic dependent launch: the prologue above (barrier init, TMEM alloc, tensor-map
+  // prefetch) overlapped the previous kernel's tail; global memory is touched only once that
+  // kernel has completed.  Our own dependents may start their prologue from here on.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   const int total = P.total_tiles;
   const int t0 = (int)(blockIdx.x >> 1);
@@ -114,6 +119,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
       int stage = 0;
       uint32_t phase = 0;
       unsigned long long st_empty = 0;
+      const int epoch = P.epoch ? *(volatile int*)P.epoch : 0;
       for (int t = t0; t < total; t += tstep) {
         TileCoord tc = tile_coord<2 * BM>(P, t);
         const Problem& pr = P.probs[tc.prob];
@@ -134,6 +140,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
           const Segment& seg = pr.segs[sg];
           const CUtensorMap* ma = &P.maps[seg.a.map];
           const CUtensorMap* mb = &P.maps[seg.b.map];
+          if (sg == pr.wait_seg && pr.wait_ctr) wait_dependency(pr, epoch);
           for (int kt = 0; kt < seg.k_tiles; ++kt, ++gs) {
             if (gs < s_lo || gs >= s_hi) continue;
             const int kblk = kt / seg.kpb;
@@ -233,6 +240,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
   if (warp == W_ALLOC) {
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
   }
+  end_epoch(P);
 }
 
 }  // namespace ppx

@@ -111,7 +111,9 @@ struct Epilogue {
   float scale;       // delta scale (1 or 1/B)
   float loss_scale;  // 0.5 or 0.5/B
   int nrep;          // plain stores only: also write every output element at out + rep_off[r] bytes
-  int pad_rep_;
+  int narrive;       // after each CTA's part of a tile is stored (incl. replicas): fence (system
+                     // scope) and add 1 to each arrive[i] (this GPU's and the peers' counters)
+  int* arrive[MAX_REP + 1];
   long long rep_off[MAX_REP];   // (peer copies of the output buffer mapped over NVLink: the phantom
                                 // all-gather fused into the compression GEMM's epilogue)
 };
@@ -130,6 +132,11 @@ struct Problem {
   int split_tiles;   //   `part`, the second half's tiles add them and run the epilogue
   float* part;       // [split_tiles][2 CTAs][128 rows][BN] fp32
   int* pflag;        // [split_tiles][2]: 1 = partial ready (set by half 0, cleared by half 1)
+  // in-kernel dependency (fused compress + all-gather + forward): before loading segment
+  // `wait_seg` the producers spin until *wait_ctr >= (*P.epoch + 1) * wait_per_epoch
+  const int* wait_ctr;
+  int wait_seg;
+  int wait_per_epoch;
   int nsegs;
   Segment segs[MAX_SEGS];
   Epilogue epi;
@@ -143,6 +150,8 @@ struct alignas(64) GemmParams {
   int total_tiles;
   int dbg;             // debug: bit0 = skip the epilogue body (TMEM drain only by arrival)
   unsigned long long* stats;   // debug (PPX_DEBUG_STATS): per-role wait / busy clock sums, else null
+  int* epoch;          // launches with waiting problems: *epoch += 1 by the last CTA to exit
+  unsigned int* done;  //   (CTA exit counter, self-resetting)
 };
 static_assert(sizeof(GemmParams) <= 32764, "kernel parameter space");
 
@@ -508,11 +517,34 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, int t) {
   TileCoord c;
   c.prob = pi;
   c.m0 = pr.m_base + mt * MT;
-  c.qn = nt / pr.npb * span;
-  c.nin = (nt - c.qn * pr.npb) * pr.BN;
+  const int qt = nt / pr.npb;     // tile column over the N blocks (a spanning tile covers `span`)
+  c.qn = qt * span;
+  c.nin = (nt - qt * pr.npb) * pr.BN;
   c.split = split;
   c.tin = local;
   return c;
+}
+
+// producer-side wait of a fused launch (see Problem::wait_ctr); TMA reads what the generic proxy
+// (local or NVLink stores) wrote, hence the proxy fence after the acquire
+__device__ __forceinline__ void wait_dependency(const Problem& pr, int epoch) {
+  const int target = (epoch + 1) * pr.wait_per_epoch;
+  int x;
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(x) : "l"(pr.wait_ctr) : "memory");
+    if (x >= target) break;
+    __nanosleep(32);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void end_epoch(const GemmParams& P) {
+  if (!P.epoch || threadIdx.x != 0) return;
+  __threadfence();
+  const unsigned int prev = atomicAdd(P.done, 1u);
+  if (prev == gridDim.x - 1) {
+    *P.done = 0u;
+    atomicAdd(P.epoch, 1);
+  }
 }
 
 __device__ __forceinline__ int op_slot(const Operand& o, int kblk, int qn) {
@@ -754,6 +786,14 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
         }
       }
     }
+    if (E.narrive) {   // publish this CTA's part of the tile (phantoms fused all-gather)
+      asm volatile("bar.sync 3, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
+      if (warp == 0 && lane == 0) {
+        __threadfence_system();
+        for (int i = 0; i < E.narrive; ++i)
+          asm volatile("red.relaxed.sys.global.add.s32 [%0], 1;" ::"l"(E.arrive[i]) : "memory");
+      }
+    }
     if (pr.ksplit > 1) {   // all epilogue warps of this CTA are done with the partial
       asm volatile("bar.sync 2, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
       if (warp == 0 && lane == 0) {
@@ -829,6 +869,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot_ptr;
+  // programmatic dependent launch: the prologue above (barrier init, TMEM alloc, tensor-map
+  // prefetch) overlapped the previous kernel's tail; global memory is touched only once that
+  // kernel has completed.  Our own dependents may start their prologue from here on.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   const int total = P.total_tiles;
 

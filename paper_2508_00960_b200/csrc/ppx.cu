@@ -41,6 +41,7 @@ struct ppx_ctx {
   int* sk_flag = nullptr;
   size_t sk_flag_cap = 0;
   unsigned int* push_arrive = nullptr;   // ppx_peer_push's CTA arrival counter (self-resetting)
+  unsigned int* fuse_done = nullptr;     // fused launches' CTA exit counter (self-resetting)
 };
 
 namespace {
@@ -172,6 +173,8 @@ struct Builder {
   // 2-SM (cta_group::2) kernel for bf16 launches whose operands tile into 64-wide atoms
   bool want_pair = false, use_pair = false;
   int BKf = 64;   // K per stage of the kernel actually launched
+  int fuse_world = 0;          // > 0: a fused compress + exchange + forward launch over this many GPUs
+  int* fuse_epoch = nullptr;
   // MN-major A (activations / deltas of the weight-gradient GEMMs) as the interleaved 5D tile
   bool use5d = getenv("PPX_NO_5D") == nullptr;
 
@@ -245,7 +248,14 @@ struct Builder {
     CUresult r = g_encode(&P.maps[P.nmaps], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(v.ptr), dims,
                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) { error(PPX_E_CUDA, "cuTensorMapEncodeTiled failed (2-SM operand map)"); return -1; }
+    if (r != CUDA_SUCCESS) {
+      char msg[256];
+      snprintf(msg, sizeof(msg), "cuTensorMapEncodeTiled failed (2-SM operand map, err %d, rank %d, dims %llu %llu %llu %llu, box %u %u %u %u, tag %d)",
+               (int)r, rank, (unsigned long long)dims[0], (unsigned long long)dims[1], (unsigned long long)dims[2],
+               (unsigned long long)dims[3], box[0], box[1], box[2], box[3], tag);
+      error(PPX_E_CUDA, msg);
+      return -1;
+    }
     map_cache[key] = P.nmaps;
     return P.nmaps++;
   }
@@ -531,7 +541,10 @@ struct Builder {
       }
     if (np > ctx->sk_part_cap || nf > ctx->sk_flag_cap) {
       cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-      if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+      if (st && (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)) {
+        cudaGetLastError();   // never leave a query's status pending for a later launch check
+        return false;
+      }
       cudaDeviceSynchronize();
       if (np > ctx->sk_part_cap) {
         if (ctx->sk_part) cudaFree(ctx->sk_part);
@@ -542,7 +555,6 @@ struct Builder {
       }
       if (nf > ctx->sk_flag_cap) {
         if (ctx->sk_flag) cudaFree(ctx->sk_flag);
-  if (ctx->push_arrive) cudaFree(ctx->push_arrive);
         ctx->sk_flag = nullptr;
         ctx->sk_flag_cap = 0;
         if (cudaMalloc(&ctx->sk_flag, nf * sizeof(int)) != cudaSuccess) { ctx->sk_flag = nullptr; return false; }
@@ -615,7 +627,15 @@ struct Builder {
     prob_bmn[ti] = prob_bmn[li];
   }
 
+  static void dbg_pending(const char* where) {
+    static const bool on = getenv("PPX_DEBUG_ERRORS") != nullptr;
+    if (!on) return;
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) fprintf(stderr, "[ppx debug] CUDA error %d pending at %s\n", (int)e, where);
+  }
+
   ppx_status launch() {
+    dbg_pending("launch entry");
     if (!ok()) return status;
     use_pair = want_pair && pair_shapes_ok();
     BKf = use_pair ? ppx::PBK : BK;
@@ -641,6 +661,7 @@ struct Builder {
         Problem& pr = P.probs[i];
         const int gran = use_pair ? (prob_bmn[i] ? 128 : 64) : (prob_bmn[i] ? CH : 32);
         if (pr.nspan > 1) {
+          if ((pr.BN / 2) % gran) continue;   // a half-width MN-major tile would split an atom per CTA
           pr.nspan = 1;
           pr.BN /= 2;
           changed = true;
@@ -667,7 +688,10 @@ struct Builder {
         for (int i = 0; i < P.nprobs; ++i) {
           Problem& pr = P.probs[i];
           const int gran = use_pair ? (prob_bmn[i] ? 128 : 64) : (prob_bmn[i] ? CH : 32);
-          if (pr.nspan > 1) { pr.nspan = 1; pr.BN /= 2; changed = true; continue; }
+          if (pr.nspan > 1) {
+            if ((pr.BN / 2) % gran) continue;
+            pr.nspan = 1; pr.BN /= 2; changed = true; continue;
+          }
           if (pr.BN / 2 >= gran && (pr.BN / 2) % gran == 0 && (pr.BN / 2) % 16 == 0 && pr.nb_extent > pr.BN / 2) {
             pr.BN /= 2;
             pr.npb = (int)cdiv(pr.nb_extent, pr.BN);
@@ -679,17 +703,30 @@ struct Builder {
         if (!changed || t2 >= t1) { memcpy(P.probs, save, sizeof(Problem) * P.nprobs); break; }
       }
     }
+    dbg_pending("before choose_ksplit");
     const bool ksplit = use_pair && choose_ksplit(ctx->num_sms / 2 - ctx->reserved_sms / 2);
+    dbg_pending("after choose_ksplit");
     if (use_pair && !ksplit && !getenv("PPX_NO_TAILSPLIT")) split_tail(ctx->num_sms / 2 - ctx->reserved_sms / 2);
     for (int i = 0; i < P.nprobs && ok(); ++i)
       for (const PendingSeg& ps : pend[i]) finalize(&P.probs[i], ps);
     if (!ok()) return status;
+    dbg_pending("after finalize");
     int tiles = 0;
     for (int i = 0; i < P.nprobs; ++i) {
       P.probs[i].tile_begin = tiles;
       tiles += ptiles(P.probs[i]);
     }
     P.total_tiles = tiles;
+    if (fuse_world) {   // fused compress + exchange + forward: arrivals per epoch on this GPU
+      if (!use_pair) return fail(ctx, PPX_E_CONFIG, "fused forward needs the 2-SM kernel (bf16, 64-aligned shapes)");
+      int ct = 0;
+      for (int i = 0; i < P.nprobs; ++i)
+        if (P.probs[i].epi.narrive) ct += ptiles(P.probs[i]);
+      for (int i = 0; i < P.nprobs; ++i)
+        if (P.probs[i].wait_ctr) P.probs[i].wait_per_epoch = fuse_world * 2 * ct;
+      P.epoch = fuse_epoch;
+      P.done = ctx->fuse_done;
+    }
     P.dbg = (getenv("PPX_DEBUG_NOEPI") ? 1 : 0) | (getenv("PPX_DEBUG_NOWAIT") ? 2 : 0);
     if (tiles == 0) return PPX_OK;
     cudaError_t e;
@@ -717,6 +754,7 @@ struct Builder {
       e = tf32 ? ppx::launch_gemm<true>(P, grid, st) : ppx::launch_gemm<false>(P, grid, st);
     }
     if (e != cudaSuccess) return fail(ctx, PPX_E_CUDA, "gemm launch: %s", cudaGetErrorString(e));
+    dbg_pending("after gemm launch");
     return PPX_OK;
   }
 };
@@ -741,8 +779,18 @@ cudaError_t launch_gemm(const GemmParams& P, int grid, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  gemm_kernel<kTF32><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(P);
-  return cudaGetLastError();
+  static const bool pdl = getenv("PPX_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, gemm_kernel<kTF32>, P);
 }
 cudaError_t launch_gemm_pair(const GemmParams& P, int grid, cudaStream_t st) {
   static bool attr_done = false;
@@ -756,13 +804,16 @@ cudaError_t launch_gemm_pair(const GemmParams& P, int grid, cudaStream_t st) {
   cfg.blockDim = dim3(NUM_THREADS, 1, 1);
   cfg.dynamicSmemBytes = PSMEM_BYTES;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  static const bool pdl = getenv("PPX_NO_PDL") == nullptr;
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see griddepcontrol in the kernel
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, gemm_pair_kernel, P);
 }
 template cudaError_t launch_gemm<true>(const GemmParams&, int, cudaStream_t);
@@ -775,6 +826,8 @@ template cudaError_t launch_gemm<false>(const GemmParams&, int, cudaStream_t);
 extern "C" {
 
 int ppx_abi_version(void) { return PPX_ABI_VERSION; }
+
+int32_t ppx_peek_error(void) { return (int32_t)cudaPeekAtLastError(); }
 
 int64_t ppx_layer_elems(int32_t s, int32_t k, int32_t p) { return Flat(s, k, p).total; }
 
@@ -795,6 +848,8 @@ ppx_status ppx_create(int32_t world, int32_t rank, int32_t device, const uint8_t
   if (cudaSetDevice(device) != cudaSuccess) { delete ctx; return PPX_E_CUDA; }
   int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0) ctx->num_sms = sms;
+  if (cudaMalloc(&ctx->fuse_done, sizeof(unsigned int)) != cudaSuccess ||
+      cudaMemset(ctx->fuse_done, 0, sizeof(unsigned int)) != cudaSuccess) { delete ctx; return PPX_E_CUDA; }
   if (world > 1) {
     if (!uid) { delete ctx; return PPX_E_CONFIG; }
     ncclUniqueId id;
@@ -813,6 +868,7 @@ ppx_status ppx_destroy(ppx_ctx* ctx) {
   if (ctx->sk_part) cudaFree(ctx->sk_part);
   if (ctx->sk_flag) cudaFree(ctx->sk_flag);
   if (ctx->push_arrive) cudaFree(ctx->push_arrive);
+  if (ctx->fuse_done) cudaFree(ctx->fuse_done);
   for (void* m : ctx->ipc_own) cudaFree(m);
   delete ctx;
   return PPX_OK;
@@ -929,6 +985,42 @@ ppx_status ppx_forward_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_i
     ppx_status s = add_forward(ctx, dt, b, io[i], B, act, phantoms, output_layer, delta_scale, loss_scale, loss);
     if (s != PPX_OK) return s;
   }
+  return b.launch();
+}
+
+// phantom.py:135-166 for the n local ranks as ONE launch: compression tiles (first in the tile
+// order) store their phantoms locally and into every peer's buffer (NVLink) and bump every GPU's
+// arrival counter; the forward tiles run their local-block K segment, then spin (producer warp)
+// until all GPUs' compression tiles of this layer have arrived, then the decompression segment.
+ppx_status ppx_forward_fused(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B, ppx_act act,
+                             void* phantoms, int32_t output_layer, float delta_scale, float loss_scale, float* loss,
+                             const ppx_exchange* ex, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (n < 1 || !io || !phantoms || !ex || !ex->arrive || !ex->wait_counter || !ex->epoch || ex->n_peers < 0 ||
+      ex->n_peers > ppx::MAX_REP || (ex->n_peers && !ex->peer_phantoms) || dt != PPX_BF16)
+    return fail(ctx, PPX_E_CONFIG, "ppx_forward_fused: bad arguments");
+  Builder b(ctx, dt, stream);
+  for (int i = 0; i < n; ++i) {
+    ppx_status st = add_compress(ctx, dt, b, io[i], B, phantoms);
+    if (st != PPX_OK) return st;
+    ppx::Epilogue& E = b.P.probs[b.P.nprobs - 1].epi;
+    E.nrep = ex->n_peers;
+    for (int r = 0; r < ex->n_peers; ++r)
+      E.rep_off[r] = (long long)((const char*)ex->peer_phantoms[r] - (const char*)phantoms);
+    E.narrive = ex->n_peers + 1;
+    for (int r = 0; r <= ex->n_peers; ++r) E.arrive[r] = ex->arrive[r];
+  }
+  for (int i = 0; i < n; ++i) {
+    ppx_status st = add_forward(ctx, dt, b, io[i], B, act, phantoms, output_layer, delta_scale, loss_scale, loss);
+    if (st != PPX_OK) return st;
+    Problem& pr = b.P.probs[b.P.nprobs - 1];
+    if (io[i].layer->p > 1) {
+      pr.wait_ctr = ex->wait_counter;
+      pr.wait_seg = 1;   // segment 0 = local block, 1 = the gathered phantoms
+    }
+  }
+  b.fuse_world = ex->n_peers + 1;
+  b.fuse_epoch = ex->epoch;
   return b.launch();
 }
 

@@ -108,12 +108,24 @@ class PhantomEngine:
         # NVLink phantom exchange (world > 1): the G buffers live in IPC-shared memory; the
         # compression GEMM stores every phantom tile into all peers' G buffers and a per-layer
         # flag replaces the NCCL all-gather (PPX_P2P=1; default NCCL)
+        # PPX_FUSED=1 (bf16): compression + all-gather + forward of a layer as ONE launch of the
+        # 2-SM kernel — compression tiles store their phantoms into every GPU's buffer over
+        # NVLink and bump per-layer arrival counters, forward tiles wait in-kernel after their
+        # local-block segment
+        self.fused = (os.environ.get("PPX_FUSED", "0") != "0" and dtype == torch.bfloat16 and s % 64 == 0
+                      and k % 64 == 0 and p // world <= 8 and not os.environ.get("PPX_NOGROUP")
+                      and (world == 1 or self._dist_ready()))
         self.p2p = int(os.environ.get("PPX_P2P", "0")) if world > 1 and self._dist_ready() else 0
+        if self.fused and world > 1 and not self.p2p:
+            self.p2p = 2
         if self.p2p:
             self.halves = 1
             self._setup_p2p(dtype)
         else:
             self.G = [torch.zeros((p, B, ldk), dtype=dtype, device=self.dev) for _ in range(L)]
+        if self.fused:
+            self.halves = 1
+            self._setup_fused()
         self.H = [torch.zeros((p, B, ldk), dtype=dtype, device=self.dev) for _ in range(L)]
         # out-of-place reduce-scatter target (world > 1): this GPU's R received slots
         self.Hr = [torch.zeros((R, B, ldk), dtype=dtype, device=self.dev) for _ in range(L)] if world > 1 else None
@@ -158,7 +170,8 @@ class PhantomEngine:
         gbytes = p * B * ldk * esz
         self._goff = [l * gbytes for l in range(L)]
         self._foff = L * gbytes
-        nbytes = self._foff + ((L * world * 4 + 255) // 256) * 256
+        self._coff = self._foff + ((L * world * 4 + 255) // 256) * 256    # per-layer arrival counters
+        nbytes = self._coff + ((L * 4 + 255) // 256) * 256
         ptr = ctypes.c_void_p()
         handle = ctypes.create_string_buffer(64)
         self.ctx.call("ppx_peer_alloc", nbytes, ctypes.byref(ptr), handle)
@@ -191,6 +204,25 @@ class PhantomEngine:
                           for l in range(L)]
         torch.cuda.synchronize()
         dist.barrier()
+
+    def _setup_fused(self):
+        L = self.L
+        self._epoch = torch.zeros(L, dtype=torch.int32, device=self.dev)
+        if self.world == 1:
+            self._arrive_local = torch.zeros(L, dtype=torch.int32, device=self.dev)
+            own = [self._arrive_local[l:].data_ptr() for l in range(L)]
+            peers = [[] for _ in range(L)]
+        else:
+            own = [self._pbase + self._coff + 4 * l for l in range(L)]
+            peers = [[self._peer_base[g] + self._coff + 4 * l for g in self._peers] for l in range(L)]
+        n = len(self._peers) if self.world > 1 else 0
+        self._ex = []
+        for l in range(L):
+            pp = (ctypes.c_void_p * max(n, 1))(*([self._peer_base[g] + self._goff[l] for g in self._peers] if n else [0]))
+            arr = (ctypes.c_void_p * (n + 1))(*([own[l]] + peers[l]))
+            vpp = ctypes.POINTER(ctypes.c_void_p)
+            ex = _lib.Exchange(n, ctypes.cast(pp, vpp), ctypes.cast(arr, vpp), own[l], self._epoch[l:].data_ptr())
+            self._ex.append((ex, pp, arr))
 
     def _init_weights(self, seed):
         """Glorot-uniform bounds of the reference init (phantom.py:126-129), drawn on device."""
@@ -290,7 +322,7 @@ class PhantomEngine:
 
     _KERNEL_CALLS = {"ppx_compress", "ppx_forward_update", "ppx_forward_output", "ppx_error_phantoms", "ppx_wgrad",
                      "ppx_backward_delta", "ppx_optimizer_step", "ppx_compress_n", "ppx_forward_n", "ppx_error_phantoms_n", "ppx_compress_push",
-                     "ppx_peer_signal", "ppx_peer_wait", "ppx_peer_push",
+                     "ppx_peer_signal", "ppx_peer_wait", "ppx_peer_push", "ppx_forward_fused",
                      "ppx_backward_delta_n"}
 
     def _call(self, name, *args):
@@ -363,6 +395,20 @@ class PhantomEngine:
                 ev.record(self.comm_stream)
                 ag_done[(l, h)] = ev
 
+        if self.fused:
+            for l in range(self.L):
+                last = train and l == self.L - 1
+                ios = []
+                for jj in range(R):
+                    kw = dict(x=self.Y[par][jj][l].data_ptr(), ld_x=s, out=self.Y[par][jj][l + 1].data_ptr(), ld_out=s)
+                    if last:
+                        kw.update(out=None if self.skip_output else kw["out"], aux=self.D[jj][0].data_ptr(), ld_aux=s,
+                                  target=self.Tgt[par][jj].data_ptr(), ld_t=s, colsum=self.gbias[jj, l].data_ptr())
+                    ios.append(self._io(jj, l, par, **kw))
+                self._call("ppx_forward_fused", pdt, R, self._ios(ios), B, self.act.code, self.G[l].data_ptr(),
+                           int(last), 1.0 / B if mean else 1.0, 0.5 / B if mean else 0.5,
+                           self.loss.data_ptr() if last else None, ctypes.byref(self._ex[l][0]), st)
+            return
         # software pipeline over batch halves: the all-gather of one half overlaps the other
         # half's GEMMs (H = 2 on multi-GPU runs; H = 1 has nothing to hide)
         for h in range(H):

@@ -124,3 +124,45 @@ def test_engine_split_k_matches_unsplit(monkeypatch):
     for a, b in zip(l0, l1):
         assert abs(a - b) <= 1e-3 * abs(a), (l0, l1)
     assert ((d1 - d0).norm() / d0.norm()).item() < 1e-2
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_engine_fused_forward_matches_oracle(graph, monkeypatch):
+    """PPX_FUSED=1: compression + (in-kernel) phantom exchange + forward of each layer as ONE
+    2-SM launch (forward tiles wait on the compression tiles' arrival counter) — bf16 steps
+    against the float64 oracle."""
+    monkeypatch.setenv("PPX_FUSED", "1")
+    n, p, k, L, B, lr = 512, 4, 64, 3, 256, 3e-3
+    eng, model, x, y = _setup(n, p, k, L, B, torch.bfloat16, "sgd", lr)
+    assert eng.fused
+    if graph:
+        eng.capture()
+    losses = []
+    for _ in range(3):
+        eng.step(graph=graph)
+        losses.append(eng.read_loss())
+    ref = _oracle_steps(model, x, y, L, 3, "sgd", lr)
+    for a, b in zip(losses, ref):
+        assert abs(a - b) <= 2e-2 * abs(b), (losses, ref)
+    for jj in range(p):
+        for l in range(L):
+            v = eng.layer_views(jj, l)
+            assert nerr(v["local"], model[jj][l]["local"]) <= 2e-2
+            assert nerr(v["compressor"], model[jj][l]["compressor"]) <= 2e-2
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_engine_pair_kernel_matches_oracle(graph):
+    """64-aligned s and k: every contraction runs on the 2-SM kernel (spanning phantom-slot tiles,
+    M < 256 weight-gradient problems) — bf16 steps against the float64 oracle."""
+    n, p, k, L, B, lr = 512, 4, 64, 3, 256, 3e-3
+    eng, model, x, y = _setup(n, p, k, L, B, torch.bfloat16, "sgd", lr)
+    if graph:
+        eng.capture()
+    losses = []
+    for _ in range(3):
+        eng.step(graph=graph)
+        losses.append(eng.read_loss())
+    ref = _oracle_steps(model, x, y, L, 3, "sgd", lr)
+    for a, b in zip(losses, ref):
+        assert abs(a - b) <= 2e-2 * abs(b), (losses, ref)

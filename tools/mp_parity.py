@@ -20,6 +20,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--graph", type=int, default=1)
     ap.add_argument("--p", type=int, default=4)
+    ap.add_argument("--k", type=int, default=32)
+    ap.add_argument("--B", type=int, default=64)
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -27,7 +29,7 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     uid = [_lib.Context.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
-    n, p, k, L, B, lr = 512, args.p, 32, 3, 64, 3e-3
+    n, p, k, L, B, lr = 512, args.p, args.k, 3, args.B, 3e-3
     dtype = torch.float32 if args.dtype == "fp32" else torch.bfloat16
     tol = 1e-4 if args.dtype == "fp32" else 2e-2
     model = po.init_phantom_model(n, p, k, L, 3)
@@ -73,7 +75,7 @@ def main():
     dist.all_reduce(w, op=dist.ReduceOp.MAX)
     if rank == 0:
         print(json.dumps({"world": world, "dtype": args.dtype, "graph": args.graph, "losses": losses, "oracle": ref,
-                          "worst_rel_err": float(w.item()), "tol": tol, "pass": float(w.item()) <= tol}), flush=True)
+                          "worst_rel_err": float(w.item()), "tol": tol, "fused": bool(eng.fused), "p2p": eng.p2p, "pass": float(w.item()) <= tol}), flush=True)
     torch.cuda.synchronize()
     dist.barrier()
     print('[teardown] closing engine', file=sys.stderr, flush=True)
