@@ -193,6 +193,7 @@ typedef struct {
   int32_t* const* arrive;        /* [n_peers + 1] arrival counters of this layer: own, then peers' */
   const int32_t* wait_counter;   /* this GPU's arrival counter of the layer (== arrive[0]) */
   int32_t* epoch;                /* this GPU's launch counter of the layer */
+  int32_t* bad;                  /* optional: |= 2 if a wait gave up after ~20 s (lost peer) */
 } ppx_exchange;
 ppx_status ppx_forward_fused(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B, ppx_act act,
                              void* phantoms, int32_t output_layer, float delta_scale, float loss_scale,

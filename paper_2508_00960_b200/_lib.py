@@ -50,7 +50,7 @@ class WgradItem(ctypes.Structure):
 class Exchange(ctypes.Structure):
     """ppx_exchange: NVLink peers and counters of one layer's fused forward launch."""
     _fields_ = [("n_peers", _i32), ("peer_phantoms", ctypes.POINTER(_vp)), ("arrive", ctypes.POINTER(_vp)),
-                ("wait_counter", _vp), ("epoch", _vp)]
+                ("wait_counter", _vp), ("epoch", _vp), ("bad", _vp)]
 
 
 class RankIO(ctypes.Structure):

@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
           const Segment& seg = pr.segs[sg];
           const CUtensorMap* ma = &P.maps[seg.a.map];
           const CUtensorMap* mb = &P.maps[seg.b.map];
-          if (sg == pr.wait_seg && pr.wait_ctr) wait_dependency(pr, epoch);
+          if (sg == pr.wait_seg && pr.wait_ctr) wait_dependency(P, pr, epoch);
           for (int kt = 0; kt < seg.k_tiles; ++kt, ++gs) {
             if (gs < s_lo || gs >= s_hi) continue;
             const int kblk = kt / seg.kpb;

@@ -152,6 +152,7 @@ struct alignas(64) GemmParams {
   unsigned long long* stats;   // debug (PPX_DEBUG_STATS): per-role wait / busy clock sums, else null
   int* epoch;          // launches with waiting problems: *epoch += 1 by the last CTA to exit
   unsigned int* done;  //   (CTA exit counter, self-resetting)
+  int* bad;            //   |= 2 when a wait timed out
 };
 static_assert(sizeof(GemmParams) <= 32764, "kernel parameter space");
 
@@ -527,12 +528,20 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, int t) {
 
 // producer-side wait of a fused launch (see Problem::wait_ctr); TMA reads what the generic proxy
 // (local or NVLink stores) wrote, hence the proxy fence after the acquire
-__device__ __forceinline__ void wait_dependency(const Problem& pr, int epoch) {
+// (bounded: after ~20 s it flags bit 1 of *P.bad and proceeds — a lost peer never hangs the GPU)
+__device__ __forceinline__ void wait_dependency(const GemmParams& P, const Problem& pr, int epoch) {
   const int target = (epoch + 1) * pr.wait_per_epoch;
   int x;
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (;;) {
     asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(x) : "l"(pr.wait_ctr) : "memory");
     if (x >= target) break;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20000000000ull) {
+      if (P.bad) atomicOr(P.bad, 2);
+      break;
+    }
     __nanosleep(32);
   }
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -743,14 +752,7 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] += (ok(i) && live) ? o[i] : 0.f;
           }
-          if (live) {
-            store32(E.out, ooff, nvalid, v);
-            for (int r = 0; r < E.nrep; ++r) {
-              Tensor2 t = E.out;
-              t.ptr = reinterpret_cast<char*>(E.out.ptr) + E.rep_off[r];
-              store32(t, ooff, nvalid, v);
-            }
-          }
+          if (live) store32(E.out, ooff, nvalid, v);
           if (flags & EP_COLSUM) {
             if (!F) {
 #pragma unroll
@@ -784,6 +786,25 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
           if (j < ncols) atomicAdd(E.colsum + tc.nin + j, cb[j]);
           cb[j] = 0.f;
         }
+      }
+    }
+    if (E.nrep && nchunks && !sp0) {
+      // replicate this CTA's finished part of the tile into the peer buffers (NVLink): the rows
+      // just stored (L2-hot) are re-read and written as consecutive 16-byte vectors by all 256
+      // epilogue threads, so every warp store is one coalesced 512-byte NVLink write
+      asm volatile("bar.sync 3, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
+      const int rbase = tc.m0 + (int)crank * BM;
+      int nrows = pr.M - rbase;
+      nrows = nrows < 0 ? 0 : (nrows > BM ? BM : nrows);
+      const int es = E.out.f32 ? 4 : 2;
+      const int upr = ncols * es / 16;
+      const long long ldb = E.out.ld * es;
+      const char* src = reinterpret_cast<const char*>(E.out.ptr) + (long long)rbase * ldb + (long long)tc.nin * es;
+      for (int u = warp * 32 + lane; u < nrows * upr; u += NUM_EPI_WARPS * 32) {
+        const int r = u / upr;
+        const long long off = r * ldb + (long long)(u - r * upr) * 16;
+        const uint4 q = *reinterpret_cast<const uint4*>(src + off);
+        for (int i = 0; i < E.nrep; ++i) *reinterpret_cast<uint4*>(const_cast<char*>(src) + E.rep_off[i] + off) = q;
       }
     }
     if (E.narrive) {   // publish this CTA's part of the tile (phantoms fused all-gather)

@@ -175,6 +175,7 @@ struct Builder {
   int BKf = 64;   // K per stage of the kernel actually launched
   int fuse_world = 0;          // > 0: a fused compress + exchange + forward launch over this many GPUs
   int* fuse_epoch = nullptr;
+  int* fuse_bad = nullptr;
   // MN-major A (activations / deltas of the weight-gradient GEMMs) as the interleaved 5D tile
   bool use5d = getenv("PPX_NO_5D") == nullptr;
 
@@ -726,6 +727,7 @@ struct Builder {
         if (P.probs[i].wait_ctr) P.probs[i].wait_per_epoch = fuse_world * 2 * ct;
       P.epoch = fuse_epoch;
       P.done = ctx->fuse_done;
+      P.bad = fuse_bad;
     }
     P.dbg = (getenv("PPX_DEBUG_NOEPI") ? 1 : 0) | (getenv("PPX_DEBUG_NOWAIT") ? 2 : 0);
     if (tiles == 0) return PPX_OK;
@@ -1021,6 +1023,7 @@ ppx_status ppx_forward_fused(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_ra
   }
   b.fuse_world = ex->n_peers + 1;
   b.fuse_epoch = ex->epoch;
+  b.fuse_bad = ex->bad;
   return b.launch();
 }
 

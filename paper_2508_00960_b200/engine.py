@@ -108,11 +108,12 @@ class PhantomEngine:
         # NVLink phantom exchange (world > 1): the G buffers live in IPC-shared memory; the
         # compression GEMM stores every phantom tile into all peers' G buffers and a per-layer
         # flag replaces the NCCL all-gather (PPX_P2P=1; default NCCL)
-        # PPX_FUSED=1 (bf16): compression + all-gather + forward of a layer as ONE launch of the
+        self.bad = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        # default (PPX_FUSED=0 disables; bf16, 64-aligned s and k): compression + all-gather + forward of a layer as ONE launch of the
         # 2-SM kernel — compression tiles store their phantoms into every GPU's buffer over
         # NVLink and bump per-layer arrival counters, forward tiles wait in-kernel after their
         # local-block segment
-        self.fused = (os.environ.get("PPX_FUSED", "0") != "0" and dtype == torch.bfloat16 and s % 64 == 0
+        self.fused = (os.environ.get("PPX_FUSED", "1") != "0" and dtype == torch.bfloat16 and s % 64 == 0
                       and k % 64 == 0 and p // world <= 8 and not os.environ.get("PPX_NOGROUP")
                       and (world == 1 or self._dist_ready()))
         self.p2p = int(os.environ.get("PPX_P2P", "0")) if world > 1 and self._dist_ready() else 0
@@ -130,7 +131,6 @@ class PhantomEngine:
         # out-of-place reduce-scatter target (world > 1): this GPU's R received slots
         self.Hr = [torch.zeros((R, B, ldk), dtype=dtype, device=self.dev) for _ in range(L)] if world > 1 else None
         self.loss = torch.zeros(1, dtype=f32, device=self.dev)
-        self.bad = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.hyper = torch.zeros(6, dtype=f32, device=self.dev)
         self.hyper_host = torch.zeros(6, dtype=f32).pin_memory()
         self.out_host = torch.zeros(1, dtype=f32).pin_memory()
@@ -221,7 +221,8 @@ class PhantomEngine:
             pp = (ctypes.c_void_p * max(n, 1))(*([self._peer_base[g] + self._goff[l] for g in self._peers] if n else [0]))
             arr = (ctypes.c_void_p * (n + 1))(*([own[l]] + peers[l]))
             vpp = ctypes.POINTER(ctypes.c_void_p)
-            ex = _lib.Exchange(n, ctypes.cast(pp, vpp), ctypes.cast(arr, vpp), own[l], self._epoch[l:].data_ptr())
+            ex = _lib.Exchange(n, ctypes.cast(pp, vpp), ctypes.cast(arr, vpp), own[l], self._epoch[l:].data_ptr(),
+                               self.bad.data_ptr())
             self._ex.append((ex, pp, arr))
 
     def _init_weights(self, seed):
@@ -602,7 +603,7 @@ class PhantomEngine:
         self.bad_host.copy_(self.bad, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         if int(self.bad_host[0]) & 2:
-            raise TrainingError("a peer GPU never published its phantoms (NVLink exchange timed out)")
+            raise TrainingError("a peer GPU never published its phantoms (NVLink exchange / fused wait timed out)")
         if int(self.bad_host[0]) != 0:
             raise TrainingError("non-finite gradient detected on the device")
         return float(self.out_host[0].item())
