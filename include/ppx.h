@@ -198,6 +198,24 @@ typedef struct {
 ppx_status ppx_forward_fused(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B, ppx_act act,
                              void* phantoms, int32_t output_layer, float delta_scale, float loss_scale,
                              float* loss, const ppx_exchange* ex, void* stream);
+/* The phantom reduce-scatter over NVLink (collectives.py:122-127, 345-357) without NCCL.
+   Sender: ppx_error_phantoms_scatter computes every slot i = sum_{local j != i} delta_j . D_{i->j}
+   (one launch, R = n = p / world local ranks); slots owned by this GPU stay in `contrib`, every
+   other slot is also copied from the epilogue into its owner g's staging area
+   stage[g] + (rank * R + i - g * R) * slot bytes, adding rows * cols / 8 per CTA part to
+   *arrive[g].  Receiver: ppx_reduce_received waits (in the kernel) until its counter reached
+   (epoch + 1) * (world - 1) * R * slot / 8, then out[j] = sum over source GPUs in ascending rank
+   order (its own contribution from `own`), and bumps *epoch.  bf16 tier. */
+typedef struct {
+  int32_t world, rank;
+  void* const* stage;       /* [world] each GPU's staging area of this layer ([world][R][B, ldk]) */
+  int32_t* const* arrive;   /* [world] each GPU's arrival counter of this layer */
+} ppx_scatter;
+ppx_status ppx_error_phantoms_scatter(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B,
+                                      void* contrib, const ppx_scatter* sc, void* stream);
+ppx_status ppx_reduce_received(ppx_ctx* ctx, ppx_dtype dt, int32_t R, int64_t slot_elems, int32_t world,
+                               int32_t rank, const void* stage, const void* own, void* out,
+                               const int32_t* counter, int32_t* epoch, int32_t* bad, void* stream);
 /* The phantom all-gather as one NVLink kernel: copies `bytes` (multiple of 16) at src to dsts[i]
    (peer mappings, same offsets) with 16-byte posted stores, then — once every CTA has fenced —
    *counter += 1 and every flags[i] = *counter (release, system scope).  Pairs with ppx_peer_wait. */

@@ -53,6 +53,11 @@ class Exchange(ctypes.Structure):
                 ("wait_counter", _vp), ("epoch", _vp), ("bad", _vp)]
 
 
+class Scatter(ctypes.Structure):
+    """ppx_scatter: owners' staging areas and arrival counters of one layer (NVLink reduce-scatter)."""
+    _fields_ = [("world", _i32), ("rank", _i32), ("stage", ctypes.POINTER(_vp)), ("arrive", ctypes.POINTER(_vp))]
+
+
 class RankIO(ctypes.Structure):
     """ppx_rank_io: one logical rank's operands in a grouped launch."""
     _fields_ = [("layer", ctypes.POINTER(Layer)), ("x", _vp), ("ld_x", _i64), ("out", _vp), ("ld_out", _i64),
@@ -99,6 +104,9 @@ _SIGS = {
     "ppx_compress_push": (_i32, [_vp, _i32, _i32, ctypes.POINTER(RankIO), _i32, _vp, _i32, ctypes.POINTER(_vp), _vp]),
     "ppx_forward_fused": (_i32, [_vp, _i32, _i32, ctypes.POINTER(RankIO), _i32, _i32, _vp, _i32, _f32, _f32, _fp,
                                    ctypes.POINTER(Exchange), _vp]),
+    "ppx_error_phantoms_scatter": (_i32, [_vp, _i32, _i32, ctypes.POINTER(RankIO), _i32, _vp, ctypes.POINTER(Scatter),
+                                           _vp]),
+    "ppx_reduce_received": (_i32, [_vp, _i32, _i32, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ppx_peer_push": (_i32, [_vp, _vp, _i64, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp]),
     "ppx_peer_signal": (_i32, [_vp, _i32, ctypes.POINTER(_vp), _vp, _vp]),
     "ppx_peer_wait": (_i32, [_vp, _i32, ctypes.POINTER(_vp), _vp, _vp, _vp]),

@@ -286,6 +286,84 @@ inline cudaError_t launch_peer_push(const void* src, long long bytes, int n, con
   return cudaGetLastError();
 }
 
+// Owner side of the NVLink reduce-scatter: wait until every source GPU's error-compression tiles
+// for this GPU's slots have arrived (wrap-safe counter >= (epoch+1) * per_epoch), then
+// out[j] = sum over source GPUs in ascending rank order of their contribution to local slot j
+// (this GPU's own contribution read from `own`, the peers' from stage[g]), fp32 sum, one rounding.
+struct ReduceArgs {
+  const __nv_bfloat16* stage;   // [world][R][slot] bf16, indexed by source GPU
+  const __nv_bfloat16* own;     // [R][slot] this GPU's contribution to its own slots
+  __nv_bfloat16* out;           // [R][slot]
+  long long slot_x8;            // R * slot elements / 8
+  long long src_stride_x8;      // R * slot / 8 (stage stride between source GPUs)
+  int world, me;
+  const int* counter;
+  int* epoch;
+  int per_epoch;
+  int* bad;
+  unsigned int* done;
+};
+__global__ void reduce_received_kernel(ReduceArgs a) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    const int target = (int)((unsigned)(*(volatile int*)a.epoch + 1) * (unsigned)a.per_epoch);
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    int x;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(x) : "l"(a.counter) : "memory");
+      if ((int)((unsigned)x - (unsigned)target) >= 0) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 20000000000ull) {
+        if (a.bad) atomicOr(a.bad, 2);
+        break;
+      }
+      __nanosleep(64);
+    }
+    ok = 1;
+  }
+  __syncthreads();
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.slot_x8; i += stride) {
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+    for (int g = 0; g < a.world; ++g) {
+      const uint4 q = g == a.me ? reinterpret_cast<const uint4*>(a.own)[i]
+                                : reinterpret_cast<const uint4*>(a.stage)[g * a.src_stride_x8 + i];
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h[e]);
+        acc[2 * e] += f.x;
+        acc[2 * e + 1] += f.y;
+      }
+    }
+    uint4 r;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&r);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
+    reinterpret_cast<uint4*>(a.out)[i] = r;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int prev = atomicAdd(a.done, 1u);
+    if (prev == gridDim.x - 1) {
+      *a.done = 0u;
+      atomicAdd(a.epoch, 1);
+    }
+  }
+  (void)ok;
+}
+inline cudaError_t launch_reduce_received(const ReduceArgs& a, cudaStream_t st) {
+  long long blocks = (a.slot_x8 + 255) / 256;
+  if (blocks > 148) blocks = 148;   // all resident: every block reads the epoch before the last bumps it
+  if (blocks < 1) blocks = 1;
+  reduce_received_kernel<<<(int)blocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
 inline cudaError_t launch_peer_signal(int n, const PeerFlags& f, int* counter, cudaStream_t st) {
   peer_signal_kernel<<<1, 32, 0, st>>>(n, f, counter);
   return cudaGetLastError();

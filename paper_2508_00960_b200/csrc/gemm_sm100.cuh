@@ -112,7 +112,8 @@ struct Epilogue {
   float loss_scale;  // 0.5 or 0.5/B
   int nrep;          // plain stores only: also write every output element at out + rep_off[r] bytes
   int narrive;       // after each CTA's part of a tile is stored (incl. replicas): fence (system
-                     // scope) and add 1 to each arrive[i] (this GPU's and the peers' counters)
+                     // scope) and add to each arrive[i] (this GPU's and the peers' counters):
+  int arrive_units;  //   0: 1 per CTA-tile; 1: rows * cols / 8 of the CTA's part (tiling-independent)
   int* arrive[MAX_REP + 1];
   long long rep_off[MAX_REP];   // (peer copies of the output buffer mapped over NVLink: the phantom
                                 // all-gather fused into the compression GEMM's epilogue)
@@ -530,13 +531,13 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, int t) {
 // (local or NVLink stores) wrote, hence the proxy fence after the acquire
 // (bounded: after ~20 s it flags bit 1 of *P.bad and proceeds — a lost peer never hangs the GPU)
 __device__ __forceinline__ void wait_dependency(const GemmParams& P, const Problem& pr, int epoch) {
-  const int target = (epoch + 1) * pr.wait_per_epoch;
+  const int target = (int)((unsigned)(epoch + 1) * (unsigned)pr.wait_per_epoch);
   int x;
   unsigned long long t0, t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (;;) {
     asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(x) : "l"(pr.wait_ctr) : "memory");
-    if (x >= target) break;
+    if ((int)((unsigned)x - (unsigned)target) >= 0) break;   // wrap-safe
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (t - t0 > 20000000000ull) {
       if (P.bad) atomicOr(P.bad, 2);
@@ -788,14 +789,14 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
         }
       }
     }
+    const int rbase = tc.m0 + (int)crank * BM;
+    int nrows = pr.M - rbase;
+    nrows = nrows < 0 ? 0 : (nrows > BM ? BM : nrows);
     if (E.nrep && nchunks && !sp0) {
       // replicate this CTA's finished part of the tile into the peer buffers (NVLink): the rows
       // just stored (L2-hot) are re-read and written as consecutive 16-byte vectors by all 256
       // epilogue threads, so every warp store is one coalesced 512-byte NVLink write
       asm volatile("bar.sync 3, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
-      const int rbase = tc.m0 + (int)crank * BM;
-      int nrows = pr.M - rbase;
-      nrows = nrows < 0 ? 0 : (nrows > BM ? BM : nrows);
       const int es = E.out.f32 ? 4 : 2;
       const int upr = ncols * es / 16;
       const long long ldb = E.out.ld * es;
@@ -811,8 +812,9 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
       asm volatile("bar.sync 3, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
       if (warp == 0 && lane == 0) {
         __threadfence_system();
+        const int amount = E.arrive_units ? nrows * ncols / 8 : 1;
         for (int i = 0; i < E.narrive; ++i)
-          asm volatile("red.relaxed.sys.global.add.s32 [%0], 1;" ::"l"(E.arrive[i]) : "memory");
+          asm volatile("red.relaxed.sys.global.add.s32 [%0], %1;" ::"l"(E.arrive[i]), "r"(amount) : "memory");
       }
     }
     if (pr.ksplit > 1) {   // all epilogue warps of this CTA are done with the partial

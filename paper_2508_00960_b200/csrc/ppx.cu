@@ -42,6 +42,7 @@ struct ppx_ctx {
   size_t sk_flag_cap = 0;
   unsigned int* push_arrive = nullptr;   // ppx_peer_push's CTA arrival counter (self-resetting)
   unsigned int* fuse_done = nullptr;     // fused launches' CTA exit counter (self-resetting)
+  unsigned int* reduce_done = nullptr;   // ppx_reduce_received's block exit counter (self-resetting)
 };
 
 namespace {
@@ -871,6 +872,7 @@ ppx_status ppx_destroy(ppx_ctx* ctx) {
   if (ctx->sk_flag) cudaFree(ctx->sk_flag);
   if (ctx->push_arrive) cudaFree(ctx->push_arrive);
   if (ctx->fuse_done) cudaFree(ctx->fuse_done);
+  if (ctx->reduce_done) cudaFree(ctx->reduce_done);
   for (void* m : ctx->ipc_own) cudaFree(m);
   delete ctx;
   return PPX_OK;
@@ -1152,9 +1154,11 @@ ppx_status ppx_error_phantoms_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx
 // ---- NVLink peer memory: the phantom all-gather as NVLink stores from the compression GEMM ----
 ppx_status ppx_peer_alloc(ppx_ctx* ctx, int64_t bytes, void** ptr, uint8_t* handle) {
   if (!ctx || bytes <= 0 || !ptr || !handle) return PPX_E_CONFIG;
-  if (!ctx->push_arrive) {   // ppx_peer_push's arrival counter (allocated here: never during capture)
+  if (!ctx->push_arrive) {   // push / reduce exit counters (allocated here: never during capture)
     CUDA_TRY(ctx, cudaMalloc(&ctx->push_arrive, sizeof(unsigned int)));
     CUDA_TRY(ctx, cudaMemset(ctx->push_arrive, 0, sizeof(unsigned int)));
+    CUDA_TRY(ctx, cudaMalloc(&ctx->reduce_done, sizeof(unsigned int)));
+    CUDA_TRY(ctx, cudaMemset(ctx->reduce_done, 0, sizeof(unsigned int)));
   }
   void* p = nullptr;
   CUDA_TRY(ctx, cudaMalloc(&p, (size_t)bytes));
@@ -1240,6 +1244,90 @@ ppx_status ppx_peer_wait(ppx_ctx* ctx, int32_t n, int32_t* const* flags, int32_t
   const char* env = getenv("PPX_PEER_TIMEOUT_S");
   const double secs = env ? atof(env) : 30.0;
   CUDA_TRY(ctx, ppx::launch_peer_wait(n, f, counter, bad, (unsigned long long)(secs * 1e9), (cudaStream_t)stream));
+  return PPX_OK;
+}
+
+// NVLink reduce-scatter, sender side (phantom.py:199-205 + collectives.py:345-357): one problem per
+// phantom slot i over this GPU's contributing ranks (as ppx_error_phantoms_n, also for n = 1); the
+// slots this GPU owns stay in `contrib`, every other slot is computed into `contrib` and copied by
+// the epilogue into its owner's staging area (sc->stage[g] + (rank * R + i - g * R) * slot) with
+// the owner's arrival counter bumped by rows * cols / 8 per CTA part.
+ppx_status ppx_error_phantoms_scatter(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B,
+                                      void* contrib, const ppx_scatter* sc, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (n < 1 || !io || B < 1 || !contrib || !sc || !sc->stage || !sc->arrive || sc->world < 1 || sc->rank < 0 ||
+      sc->rank >= sc->world || dt != PPX_BF16 || n > ppx::MAX_SEGS)
+    return fail(ctx, PPX_E_CONFIG, "ppx_error_phantoms_scatter: bad arguments");
+  const int p = io[0].layer->p, s = io[0].layer->s, k = io[0].layer->k;
+  for (int j = 0; j < n; ++j) {
+    const ppx_layer* L = io[j].layer;
+    if (bad_layer(L) || !io[j].x || L->s != s || L->k != k || L->p != p || (j && L->rank <= io[j - 1].layer->rank))
+      return fail(ctx, PPX_E_CONFIG, "ppx_error_phantoms_scatter: ranks must share (s, k, p) and ascend");
+  }
+  if (p < 2) return PPX_OK;
+  if (p % sc->world || p / sc->world != n) return fail(ctx, PPX_E_CONFIG, "ppx_error_phantoms_scatter: R != p / world");
+  Flat f(s, k, p);
+  const int R = n, es = 2;
+  const int64_t slot_bytes = (int64_t)B * f.ldk * es;
+  int i = 0;
+  while (i < p) {
+    Builder b(ctx, dt, stream);
+    const int kt = (int)cdiv(s, b.BK);
+    for (; i < p && b.P.nprobs < ppx::MAX_PROBS - 1; ++i) {
+      int nseg = 0;
+      for (int j = 0; j < n; ++j) nseg += io[j].layer->rank != i;
+      if (!nseg) continue;
+      Problem* pr = b.new_problem(B, k, 1, true);
+      for (int j = 0; j < n; ++j) {
+        const ppx_layer* L = io[j].layer;
+        if (L->rank == i) continue;
+        Opnd a{view2(io[j].x, B, s, io[j].ld_x)};
+        Opnd d{view3(elem(dt, L->w, f.dec), p - 1, s, k, f.ldk, (int64_t)s * f.ldk)};
+        d.mn = 1;
+        d.slot_base = i - (i > L->rank ? 1 : 0);
+        b.add_segment(pr, a, d, kt, kt);
+      }
+      if (!pr) break;
+      char* local = (char*)contrib + (int64_t)i * slot_bytes;
+      pr->epi.out = t2(local, f.ldk, 0);
+      const int g = i / R;
+      if (g != sc->rank) {
+        char* dst = (char*)sc->stage[g] + ((int64_t)sc->rank * R + (i - g * R)) * slot_bytes;
+        pr->epi.nrep = 1;
+        pr->epi.rep_off[0] = (long long)(dst - local);
+        pr->epi.narrive = 1;
+        pr->epi.arrive_units = 1;
+        pr->epi.arrive[0] = sc->arrive[g];
+      }
+    }
+    ppx_status st = b.launch();
+    if (st != PPX_OK) return st;
+  }
+  return PPX_OK;
+}
+
+ppx_status ppx_reduce_received(ppx_ctx* ctx, ppx_dtype dt, int32_t R, int64_t slot_elems, int32_t world, int32_t rank,
+                               const void* stage, const void* own, void* out, const int32_t* counter, int32_t* epoch,
+                               int32_t* bad, void* stream) {
+  if (!ctx || !stage || !own || !out || !counter || !epoch || R < 1 || world < 1 || rank < 0 || rank >= world ||
+      slot_elems % 8 || dt != PPX_BF16)
+    return fail(ctx, PPX_E_CONFIG, "ppx_reduce_received: bad arguments");
+  if (!ctx->reduce_done) return fail(ctx, PPX_E_SEQUENCING, "ppx_reduce_received before ppx_peer_alloc");
+  ppx::ReduceArgs a;
+  a.stage = (const __nv_bfloat16*)stage;
+  a.own = (const __nv_bfloat16*)own;
+  a.out = (__nv_bfloat16*)out;
+  a.slot_x8 = R * slot_elems / 8;
+  a.src_stride_x8 = R * slot_elems / 8;
+  a.world = world;
+  a.me = rank;
+  a.counter = counter;
+  a.epoch = epoch;
+  a.per_epoch = 0;   // set below: (world - 1) sources x R slots x slot elements / 8
+  a.per_epoch = (int)((int64_t)(world - 1) * R * slot_elems / 8);
+  a.bad = bad;
+  a.done = ctx->reduce_done;
+  CUDA_TRY(ctx, ppx::launch_reduce_received(a, (cudaStream_t)stream));
   return PPX_OK;
 }
 

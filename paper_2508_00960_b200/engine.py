@@ -171,7 +171,10 @@ class PhantomEngine:
         self._goff = [l * gbytes for l in range(L)]
         self._foff = L * gbytes
         self._coff = self._foff + ((L * world * 4 + 255) // 256) * 256    # per-layer arrival counters
-        nbytes = self._coff + ((L * 4 + 255) // 256) * 256
+        self._rcoff = self._coff + ((L * 4 + 255) // 256) * 256           # reduce-scatter arrival counters
+        sbytes = world * self.R * B * ldk * esz                           # reduce-scatter staging per layer
+        self._soff = [self._rcoff + ((L * 4 + 255) // 256) * 256 + l * sbytes for l in range(L)]
+        nbytes = self._soff[0] + L * sbytes
         ptr = ctypes.c_void_p()
         handle = ctypes.create_string_buffer(64)
         self.ctx.call("ppx_peer_alloc", nbytes, ctypes.byref(ptr), handle)
@@ -202,6 +205,21 @@ class PhantomEngine:
                          for l in range(L)]
         self._wait_src = [mk([self._pbase + self._foff + 4 * (l * world + g) for g in self._peers])
                           for l in range(L)]
+        # NVLink reduce-scatter (bf16, with the IPC region): default when a GPU owns >= 2 logical
+        # ranks (C3 on 4 GPUs: 5.41 -> 5.31 ms); with one rank per GPU the per-slot error
+        # compression tiles worse than the NCCL path (C2 on 4 GPUs: 2.53 -> 2.70 ms), so it is
+        # opt-in there (PPX_NVRS=1; PPX_NVRS=0 always NCCL)
+        nv = os.environ.get("PPX_NVRS", "")
+        self.nvrs = dtype == torch.bfloat16 and self.R <= 8 and (nv == "1" or (nv == "" and self.R >= 2))
+        if self.nvrs:
+            vpp = ctypes.POINTER(ctypes.c_void_p)
+            base = lambda g: self._pbase if g == self.rank else self._peer_base[g]   # noqa: E731
+            self._rsepoch = torch.zeros(L, dtype=torch.int32, device=self.dev)
+            self._sc = []
+            for l in range(L):
+                st = (ctypes.c_void_p * world)(*[base(g) + self._soff[l] for g in range(world)])
+                ar = (ctypes.c_void_p * world)(*[base(g) + self._rcoff + 4 * l for g in range(world)])
+                self._sc.append((_lib.Scatter(world, self.rank, ctypes.cast(st, vpp), ctypes.cast(ar, vpp)), st, ar))
         torch.cuda.synchronize()
         dist.barrier()
 
@@ -324,6 +342,7 @@ class PhantomEngine:
     _KERNEL_CALLS = {"ppx_compress", "ppx_forward_update", "ppx_forward_output", "ppx_error_phantoms", "ppx_wgrad",
                      "ppx_backward_delta", "ppx_optimizer_step", "ppx_compress_n", "ppx_forward_n", "ppx_error_phantoms_n", "ppx_compress_push",
                      "ppx_peer_signal", "ppx_peer_wait", "ppx_peer_push", "ppx_forward_fused",
+                     "ppx_error_phantoms_scatter", "ppx_reduce_received",
                      "ppx_backward_delta_n"}
 
     def _call(self, name, *args):
@@ -447,7 +466,13 @@ class PhantomEngine:
         esz = self.H[0].element_size()
         cur = 0
         for l in range(L - 1, -1, -1):
-            if self.group >= R and not os.environ.get("PPX_K3_PERRANK"):
+            if getattr(self, "nvrs", False) and self.p2p:
+                # NVLink reduce-scatter: the error-compression epilogue copies every peer-owned
+                # slot into its owner's staging area; reduced after the weight gradients
+                ios = [self._io(jj, l, par, x=self.D[jj][cur].data_ptr(), ld_x=s) for jj in range(R)]
+                self._call("ppx_error_phantoms_scatter", pdt, R, self._ios(ios), B, self.H[l].data_ptr(),
+                           ctypes.byref(self._sc[l][0]), st)
+            elif self.group >= R and not os.environ.get("PPX_K3_PERRANK"):
                 # one launch: slot i = sum_{local j != i} delta_j . D_{i->j}, every slot with a
                 # contributor overwritten (with R = 1 the own slot has none and stays zero: the
                 # reduce-scatter is out of place)
@@ -458,7 +483,8 @@ class PhantomEngine:
                 for jj in range(R):
                     self._call("ppx_error_phantoms", pdt, ctypes.byref(self._layer(jj, l, par)), B,
                                self.D[jj][cur].data_ptr(), s, self.H[l].data_ptr(), 1, st)
-            if self.world > 1 and not self._dbg_skip_rs:
+            nvrs = getattr(self, "nvrs", False) and self.p2p
+            if self.world > 1 and not self._dbg_skip_rs and not nvrs:
                 self._join(S, self.comm_stream)
                 self._call("ppx_reduce_scatter_to", pdt, self.H[l].data_ptr(), self.Hr[l].data_ptr(), slot, R,
                            self.comm_stream.cuda_stream)
@@ -487,8 +513,13 @@ class PhantomEngine:
                 self._launch_wgrad([it for chunk in per_rank[c:c + per] for it in chunk], st)
             if self.world > 1 and self.comm_sms:
                 self.ctx.call("ppx_set_reserved_sms", 0)
-            if self.world > 1:
+            if self.world > 1 and not nvrs:
                 self._join(self.comm_stream, S)
+            if nvrs:
+                own = self.H[l].data_ptr() + self.rank * R * slot * esz
+                self._call("ppx_reduce_received", pdt, R, slot, self.world, self.rank, self._pbase + self._soff[l], own,
+                           self.Hr[l].data_ptr(), self._pbase + self._rcoff + 4 * l, self._rsepoch[l:].data_ptr(),
+                           self.bad.data_ptr(), st)
             if l > 0:
                 ios = []
                 for jj in range(R):

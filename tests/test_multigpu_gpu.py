@@ -26,16 +26,19 @@ def test_engine_two_gpus_matches_oracle(dtype, p, p2p):
     assert '"pass": true' in r.stdout
 
 
+@pytest.mark.parametrize("nvrs", ["1", "0"])
 @pytest.mark.parametrize("p", [2, 4])
-def test_engine_two_gpus_fused_forward(p):
+def test_engine_two_gpus_fused_forward(p, nvrs):
     """PPX_FUSED=1 over 2 GPUs: the compression tiles store into the peer's phantom buffer over
-    NVLink and bump both GPUs' arrival counters; forward tiles wait in-kernel (bf16, k = 64)."""
+    NVLink and bump both GPUs' arrival counters; forward tiles wait in-kernel (bf16, k = 64).
+    nvrs=1: the reduce-scatter too (error-compression epilogue -> owner staging -> in-kernel wait
+    and ascending-rank sum); nvrs=0: NCCL reduce-scatter."""
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29534", os.path.join(ROOT, "tools", "mp_parity.py"),
+           "--master-addr", "127.0.0.1", "--master-port", str(29534 + int(nvrs)), os.path.join(ROOT, "tools", "mp_parity.py"),
            "--dtype", "bf16", "--p", str(p), "--k", "64", "--B", "256"]
-    env = dict(os.environ, PPX_FUSED="1")
+    env = dict(os.environ, PPX_FUSED="1", PPX_NVRS=nvrs)
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert '"pass": true' in r.stdout and '"fused": true' in r.stdout
