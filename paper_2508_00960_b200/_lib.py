@@ -149,6 +149,8 @@ def load():
                     f"{LIB_PATH} is missing; run __graft_entry__.build() (no CPU fallback exists)")
             lib = ctypes.CDLL(LIB_PATH)
             for name, (res, args) in _SIGS.items():
+                if os.environ.get("PPX_LIB") and not hasattr(lib, name):
+                    continue   # A/B runs against an older build (PPX_LIB): bind what it exports
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args

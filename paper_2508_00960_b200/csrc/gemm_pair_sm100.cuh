@@ -113,7 +113,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
     epilogue_loop<2 * BM, true>(P, tmem_base, tfull_bar(0), tempty_bar(0), t0, tstep, crank, warp, lane, cs_smem);
   } else {
   reg_dealloc_mainloop();
-  if (warp == W_TMA) {
+  if (warp >= W_PUB0) {
+    publisher_loop<2 * BM>(P, t0, tstep, crank, warp, lane);
+  } else if (warp == W_TMA) {
     // ===================== TMA producer (both CTAs) =====================
     if (lane == 0) {
       int stage = 0;
@@ -131,18 +133,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
         const bool span = pr.nspan > 1;
         const int bn0 = span ? tc.nin : tc.nin + (int)crank * bnc;
         const int qb = span ? tc.qn + (int)crank : tc.qn;
-        int s_lo = 0, s_hi = 1 << 30, gs = 0;
-        if (pr.ksplit > 1) {
-          if (tc.split == 0) s_hi = pr.kst_total / 2;
-          else s_lo = pr.kst_total / 2;
-        }
         for (int sg = 0; sg < pr.nsegs; ++sg) {
           const Segment& seg = pr.segs[sg];
           const CUtensorMap* ma = &P.maps[seg.a.map];
           const CUtensorMap* mb = &P.maps[seg.b.map];
           if (sg == pr.wait_seg && pr.wait_ctr) wait_dependency(P, pr, epoch);
-          for (int kt = 0; kt < seg.k_tiles; ++kt, ++gs) {
-            if (gs < s_lo || gs >= s_hi) continue;
+          for (int kt = 0; kt < seg.k_tiles; ++kt) {
             const int kblk = kt / seg.kpb;
             const int kin = (kt - kblk * seg.kpb) * PBK;
             mbar_wait_t(empty_bar(stage), phase ^ 1u, kStats && P.stats != nullptr, st_empty);
@@ -183,11 +179,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
         const uint32_t tmem_d = tmem_base + as * BN_MAX;
         const int bnc = pr.BN / 2;
         uint32_t accum = 0;
-        int s_lo = 0, s_hi = 1 << 30, gs = 0;
-        if (pr.ksplit > 1) {
-          if (tc.split == 0) s_hi = pr.kst_total / 2;
-          else s_lo = pr.kst_total / 2;
-        }
         for (int sg = 0; sg < pr.nsegs; ++sg) {
           const Segment& seg = pr.segs[sg];
           const uint32_t idesc = seg.idesc;
@@ -201,8 +192,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
           else if (seg.b.atoms4d == 2) {
             b_lbo = 1024; b_sbo = (bnc / CHA) * 1024; b_step = 2 * b_sbo; b_katom = 4 * b_step;
           } else { b_lbo = PBK * ROW_BYTES; b_sbo = 1024; b_step = KMMA * ROW_BYTES; b_katom = 4 * b_step; }
-          for (int kt = 0; kt < seg.k_tiles; ++kt, ++gs) {
-            if (gs < s_lo || gs >= s_hi) continue;
+          for (int kt = 0; kt < seg.k_tiles; ++kt) {
             mbar_wait_t(full_bar(stage), phase, kStats && P.stats != nullptr, st_full);
             tc_fence_after();
             const uint32_t da = sA + stage * PA_STAGE;

@@ -128,11 +128,6 @@ struct Problem {
   int m_base;        // first row covered by this problem's tiles (a split-off tail of a problem)
   int nspan;         // 2-SM kernel: N blocks per tile (2 = each CTA of the pair owns one whole N block)
   int tile_begin;    // prefix over problems
-  int ksplit;        // 2-SM kernel: 2 = K split in two halves; tiles [0, split_tiles) run the first
-  int kst_total;     //   half (stages [0, kst_total/2) over all segments) and park fp32 partials in
-  int split_tiles;   //   `part`, the second half's tiles add them and run the epilogue
-  float* part;       // [split_tiles][2 CTAs][128 rows][BN] fp32
-  int* pflag;        // [split_tiles][2]: 1 = partial ready (set by half 0, cleared by half 1)
   // in-kernel dependency (fused compress + all-gather + forward): before loading segment
   // `wait_seg` the producers spin until *wait_ctr >= (*P.epoch + 1) * wait_per_epoch
   const int* wait_ctr;
@@ -497,7 +492,6 @@ __device__ __forceinline__ float warp_transpose_sum(float* v, int lane) {
 // ------------------------------------------------------------------------------------------
 struct TileCoord {
   int prob, m0, qn, nin;
-  int split, tin;    // K half of a split problem and the tile's index inside its half
 };
 
 template <int MT>
@@ -507,11 +501,6 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, int t) {
   while (pi + 1 < P.nprobs && t >= P.probs[pi + 1].tile_begin) ++pi;
   const Problem& pr = P.probs[pi];
   int local = t - pr.tile_begin;
-  int split = 0;
-  if (pr.ksplit > 1 && local >= pr.split_tiles) {
-    split = 1;
-    local -= pr.split_tiles;
-  }
   const int span = pr.nspan > 1 ? pr.nspan : 1;
   int ntn = (pr.nblk + span - 1) / span * pr.npb;
   int mt = local / ntn;
@@ -522,8 +511,6 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, int t) {
   const int qt = nt / pr.npb;     // tile column over the N blocks (a spanning tile covers `span`)
   c.qn = qt * span;
   c.nin = (nt - qt * pr.npb) * pr.BN;
-  c.split = split;
-  c.tin = local;
   return c;
 }
 
@@ -565,6 +552,50 @@ __device__ __forceinline__ int op_slot(const Operand& o, int kblk, int qn) {
 // ------------------------------------------------------------------------------------------
 // epilogue warps (4 warps = the 4 TMEM lane quadrants): drain one accumulator stage per tile
 // ------------------------------------------------------------------------------------------
+// NVLink exchange tiles (compression / error compression with peer replicas or arrival counters)
+// are published by the two otherwise idle warps (10, 11) while the epilogue warps move on: after
+// storing such a tile the epilogue warps meet them at a named barrier; the publisher warps re-read the stored
+// rows (L2-hot) and write them to every replica as consecutive 16-byte vectors (coalesced NVLink
+// writes), then fence at system scope and bump the arrival counters.
+constexpr int W_PUB0 = 10;
+__device__ __forceinline__ bool publishes(const Epilogue& E) { return E.nrep || E.narrive; }
+
+template <int MT>
+__device__ __forceinline__ void publisher_loop(const GemmParams& P, int t0, int tstep, uint32_t crank, int warp,
+                                               int lane) {
+  const int tid = (warp - W_PUB0) * 32 + lane;
+  for (int t = t0; t < P.total_tiles; t += tstep) {
+    TileCoord tc = tile_coord<MT>(P, t);
+    const Problem& pr = P.probs[tc.prob];
+    const Epilogue& E = pr.epi;
+    if (!publishes(E)) continue;
+    asm volatile("bar.sync 4, %0;" ::"n"(NUM_EPI_WARPS * 32 + 64) : "memory");
+    const int rbase = tc.m0 + (int)crank * BM;
+    int nrows = pr.M - rbase;
+    nrows = nrows < 0 ? 0 : (nrows > BM ? BM : nrows);
+    const int ncols = pr.nb_extent - tc.nin < pr.BN ? pr.nb_extent - tc.nin : pr.BN;
+    if (E.nrep) {
+      const int es = E.out.f32 ? 4 : 2;
+      const int upr = ncols * es / 16;
+      const long long ldb = E.out.ld * es;
+      const char* src = reinterpret_cast<const char*>(E.out.ptr) + (long long)rbase * ldb + (long long)tc.nin * es;
+      for (int u = tid; u < nrows * upr; u += 64) {
+        const int r = u / upr;
+        const long long off = r * ldb + (long long)(u - r * upr) * 16;
+        const uint4 q = *reinterpret_cast<const uint4*>(src + off);
+        for (int i = 0; i < E.nrep; ++i) *reinterpret_cast<uint4*>(const_cast<char*>(src) + E.rep_off[i] + off) = q;
+      }
+    }
+    asm volatile("bar.sync 5, 64;" ::: "memory");
+    if (E.narrive && tid == 0) {
+      __threadfence_system();
+      const int amount = E.arrive_units ? nrows * ncols / 8 : 1;
+      for (int i = 0; i < E.narrive; ++i)
+        asm volatile("red.relaxed.sys.global.add.s32 [%0], %1;" ::"l"(E.arrive[i]), "r"(amount) : "memory");
+    }
+  }
+}
+
 template <int MT, bool kPair>
 __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem_base, uint32_t tfull0,
                                               uint32_t tempty0, int t0, int tstep, uint32_t crank, int warp,
@@ -587,13 +618,7 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
     rows_valid = rows_valid < 0 ? 0 : (rows_valid > 32 ? 32 : rows_valid);
     const int row = row0 + lane;
     const bool row_ok = lane < rows_valid;
-    // split-K: the first half only parks its raw accumulators; the second half adds them first
-    const bool sp0 = pr.ksplit > 1 && tc.split == 0;
-    const bool sp1 = pr.ksplit > 1 && tc.split == 1;
-    float* const part = pr.ksplit > 1 ? pr.part + ((size_t)(tc.tin * 2 + (int)crank) * BM + wq * 32 + lane) * pr.BN
-                                      : nullptr;
-    int* const pflag = pr.ksplit > 1 ? pr.pflag + tc.tin * 2 + (int)crank : nullptr;
-    const uint32_t flags = sp0 ? 0u : E.flags;
+    const uint32_t flags = E.flags;
     const bool upd = (flags & (EP_SGD | EP_ADAM)) != 0;
     // per-row input streamed one chunk ahead: target | fp32 master | ReLU mask | accumulated output
     const Tensor2* sa = (flags & EP_LOSS) ? &E.target
@@ -632,12 +657,6 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
     mbar_wait_t(tfull_bar(as), aphase, kStats && P.stats != nullptr, st_wait);
     const unsigned long long c_busy = kStats && P.stats ? clock64() : 0ull;
     tc_fence_after();
-    if (sp1) {   // the partner tile (lower index, so scheduled no later) publishes its partial
-      int x;
-      do {
-        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(x) : "l"(pflag) : "memory");
-      } while (x == 0);
-    }
     float loss_acc = 0.f;
     bool bad = false;
     Pre32 pa;
@@ -666,24 +685,6 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
       const unsigned long long c_t0 = kStats && P.stats ? clock64() : 0ull;
       tmem_ld32(tmem_base + as * BN_MAX + c * 32 + ((uint32_t)(wq * 32) << 16), v);
       if (kStats && P.stats) st_tmem += clock64() - c_t0;
-      if (sp0) {
-        float4* q = reinterpret_cast<float4*>(part + c * 32);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) q[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        pa = na;
-        continue;
-      }
-      if (sp1) {
-        const float4* q = reinterpret_cast<const float4*>(part + c * 32);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float4 w4 = q[i];
-          v[4 * i] += w4.x;
-          v[4 * i + 1] += w4.y;
-          v[4 * i + 2] += w4.z;
-          v[4 * i + 3] += w4.w;
-        }
-      }
       // full chunks (every row and column valid, the common case) compile without per-element masks
       auto body = [&](auto full_c) {
         constexpr bool F = decltype(full_c)::value;
@@ -789,45 +790,9 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
         }
       }
     }
-    const int rbase = tc.m0 + (int)crank * BM;
-    int nrows = pr.M - rbase;
-    nrows = nrows < 0 ? 0 : (nrows > BM ? BM : nrows);
-    if (E.nrep && nchunks && !sp0) {
-      // replicate this CTA's finished part of the tile into the peer buffers (NVLink): the rows
-      // just stored (L2-hot) are re-read and written as consecutive 16-byte vectors by all 256
-      // epilogue threads, so every warp store is one coalesced 512-byte NVLink write
-      asm volatile("bar.sync 3, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
-      const int es = E.out.f32 ? 4 : 2;
-      const int upr = ncols * es / 16;
-      const long long ldb = E.out.ld * es;
-      const char* src = reinterpret_cast<const char*>(E.out.ptr) + (long long)rbase * ldb + (long long)tc.nin * es;
-      for (int u = warp * 32 + lane; u < nrows * upr; u += NUM_EPI_WARPS * 32) {
-        const int r = u / upr;
-        const long long off = r * ldb + (long long)(u - r * upr) * 16;
-        const uint4 q = *reinterpret_cast<const uint4*>(src + off);
-        for (int i = 0; i < E.nrep; ++i) *reinterpret_cast<uint4*>(const_cast<char*>(src) + E.rep_off[i] + off) = q;
-      }
-    }
-    if (E.narrive) {   // publish this CTA's part of the tile (phantoms fused all-gather)
-      asm volatile("bar.sync 3, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
-      if (warp == 0 && lane == 0) {
-        __threadfence_system();
-        const int amount = E.arrive_units ? nrows * ncols / 8 : 1;
-        for (int i = 0; i < E.narrive; ++i)
-          asm volatile("red.relaxed.sys.global.add.s32 [%0], %1;" ::"l"(E.arrive[i]), "r"(amount) : "memory");
-      }
-    }
-    if (pr.ksplit > 1) {   // all epilogue warps of this CTA are done with the partial
-      asm volatile("bar.sync 2, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
-      if (warp == 0 && lane == 0) {
-        if (sp0) {
-          __threadfence();
-          asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(pflag), "r"(1) : "memory");
-        } else {
-          asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(pflag), "r"(0) : "memory");
-        }
-      }
-    }
+    // hand the stored tile to the publisher warps (a full barrier: it also waits until they took
+    // the previous published tile, so barrier generations never mix)
+    if (publishes(E)) asm volatile("bar.sync 4, %0;" ::"n"(NUM_EPI_WARPS * 32 + 64) : "memory");
     tc_fence_before();
     __syncwarp();
     if (lane == 0) {
@@ -906,7 +871,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
                              cs_smem);
   } else {
   reg_dealloc_mainloop();
-  if (warp == W_TMA) {
+  if (warp >= W_PUB0) {
+    publisher_loop<BM>(P, blockIdx.x, gridDim.x, 0u, warp, lane);
+  } else if (warp == W_TMA) {
     // ===================== TMA producer =====================
     if (lane == 0) {
       int stage = 0;

@@ -34,12 +34,6 @@ struct ppx_ctx {
   std::vector<std::pair<char*, size_t>> ws;
   std::vector<void*> ipc_own;      // ppx_peer_alloc regions (cudaFree at destroy)
   std::vector<void*> ipc_mapped;   // ppx_peer_open mappings (cudaIpcCloseMemHandle at destroy)
-  // split-K partials and ready flags of the 2-SM kernel (flags self-reset: one split launch in
-  // flight per ctx, i.e. split GEMMs of one ctx must share a stream)
-  float* sk_part = nullptr;
-  size_t sk_part_cap = 0;
-  int* sk_flag = nullptr;
-  size_t sk_flag_cap = 0;
   unsigned int* push_arrive = nullptr;   // ppx_peer_push's CTA arrival counter (self-resetting)
   unsigned int* fuse_done = nullptr;     // fused launches' CTA exit counter (self-resetting)
   unsigned int* reduce_done = nullptr;   // ppx_reduce_received's block exit counter (self-resetting)
@@ -502,82 +496,9 @@ struct Builder {
 
   static int ptiles(const Problem& pr) {
     const int span = pr.nspan > 1 ? pr.nspan : 1;
-    return pr.m_tiles * (int)cdiv(pr.nblk, span) * pr.npb * (pr.ksplit > 1 ? 2 : 1);
+    return pr.m_tiles * (int)cdiv(pr.nblk, span) * pr.npb;
   }
 
-  // Split-K for launches too small to fill the GPU (e.g. one logical rank's weight gradients:
-  // ~100 long tiles on 74 clusters = 2 rounds, the second 40% full): when a simulation of the
-  // static round-robin schedule says halving every long problem's K finishes >10% sooner, each
-  // such problem runs its tiles twice (first / second K half); the second half adds the first
-  // half's fp32 partial and runs the real epilogue.
-  bool choose_ksplit(int C) {
-    // measured on B200 (one logical rank's weight gradients, 104 tiles): the extra tile
-    // prologues / exposed epilogues outweigh the better rounds, so it is opt-in (PPX_SPLITK=1)
-    if (C < 1 || !getenv("PPX_SPLITK") || getenv("PPX_NO_SPLITK")) return false;
-    int kst[ppx::MAX_PROBS], bt[ppx::MAX_PROBS];
-    for (int i = 0; i < P.nprobs; ++i) {
-      kst[i] = 0;
-      for (const PendingSeg& ps : pend[i]) kst[i] += (int)cdiv(ps.kext, ppx::PBK) * ps.nkblk;
-      bt[i] = ptiles(P.probs[i]);
-    }
-    auto sim = [&](bool sp) {
-      std::vector<double> load(C, 0.0);
-      int t = 0;
-      for (int i = 0; i < P.nprobs; ++i) {
-        const bool el = sp && kst[i] >= 16;
-        for (int h = 0; h < (el ? 2 : 1); ++h) {
-          const double cost = el ? kst[i] / 2.0 + 6.0 : kst[i] + 4.0;
-          for (int j = 0; j < bt[i]; ++j) load[t++ % C] += cost;
-        }
-      }
-      double m = 0;
-      for (double x : load) m = x > m ? x : m;
-      return m;
-    };
-    if (sim(true) >= 0.9 * sim(false)) return false;
-    size_t nf = 0, np = 0;
-    for (int i = 0; i < P.nprobs; ++i)
-      if (kst[i] >= 16) {
-        nf += 2 * (size_t)bt[i];
-        np += 2 * (size_t)bt[i] * ppx::BM * P.probs[i].BN;
-      }
-    if (np > ctx->sk_part_cap || nf > ctx->sk_flag_cap) {
-      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-      if (st && (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)) {
-        cudaGetLastError();   // never leave a query's status pending for a later launch check
-        return false;
-      }
-      cudaDeviceSynchronize();
-      if (np > ctx->sk_part_cap) {
-        if (ctx->sk_part) cudaFree(ctx->sk_part);
-        ctx->sk_part = nullptr;
-        ctx->sk_part_cap = 0;
-        if (cudaMalloc(&ctx->sk_part, np * sizeof(float)) != cudaSuccess) { ctx->sk_part = nullptr; return false; }
-        ctx->sk_part_cap = np;
-      }
-      if (nf > ctx->sk_flag_cap) {
-        if (ctx->sk_flag) cudaFree(ctx->sk_flag);
-        ctx->sk_flag = nullptr;
-        ctx->sk_flag_cap = 0;
-        if (cudaMalloc(&ctx->sk_flag, nf * sizeof(int)) != cudaSuccess) { ctx->sk_flag = nullptr; return false; }
-        if (cudaMemset(ctx->sk_flag, 0, nf * sizeof(int)) != cudaSuccess) return false;
-        ctx->sk_flag_cap = nf;
-      }
-    }
-    size_t fo = 0, po = 0;
-    for (int i = 0; i < P.nprobs; ++i) {
-      Problem& pr = P.probs[i];
-      if (kst[i] < 16) continue;
-      pr.ksplit = 2;
-      pr.kst_total = kst[i];
-      pr.split_tiles = bt[i];
-      pr.part = ctx->sk_part + po;
-      pr.pflag = ctx->sk_flag + fo;
-      po += 2 * (size_t)bt[i] * ppx::BM * pr.BN;
-      fo += 2 * (size_t)bt[i];
-    }
-    return true;
-  }
 
   // 2-SM kernel: a problem whose N blocks (slots) are each at most half a tile wide runs tiles
   // that span two consecutive blocks, one per CTA (e.g. the 7 k-wide phantom slots of
@@ -705,10 +626,7 @@ struct Builder {
         if (!changed || t2 >= t1) { memcpy(P.probs, save, sizeof(Problem) * P.nprobs); break; }
       }
     }
-    dbg_pending("before choose_ksplit");
-    const bool ksplit = use_pair && choose_ksplit(ctx->num_sms / 2 - ctx->reserved_sms / 2);
-    dbg_pending("after choose_ksplit");
-    if (use_pair && !ksplit && !getenv("PPX_NO_TAILSPLIT")) split_tail(ctx->num_sms / 2 - ctx->reserved_sms / 2);
+    if (use_pair && !getenv("PPX_NO_TAILSPLIT")) split_tail(ctx->num_sms / 2 - ctx->reserved_sms / 2);
     for (int i = 0; i < P.nprobs && ok(); ++i)
       for (const PendingSeg& ps : pend[i]) finalize(&P.probs[i], ps);
     if (!ok()) return status;
@@ -868,8 +786,6 @@ ppx_status ppx_destroy(ppx_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (auto& c : ctx->ws) cudaFree(c.first);
   for (void* m : ctx->ipc_mapped) cudaIpcCloseMemHandle(m);
-  if (ctx->sk_part) cudaFree(ctx->sk_part);
-  if (ctx->sk_flag) cudaFree(ctx->sk_flag);
   if (ctx->push_arrive) cudaFree(ctx->push_arrive);
   if (ctx->fuse_done) cudaFree(ctx->fuse_done);
   if (ctx->reduce_done) cudaFree(ctx->reduce_done);

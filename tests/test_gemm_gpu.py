@@ -88,22 +88,3 @@ def test_error_phantoms_grouped(dtype, s, k, p, R, B):
         err = ((got - ref).norm() / ref.norm()).item()
         tol = 1e-5 if dtype == torch.float32 else 1e-2   # bf16 output rounding
         assert err < tol, (i, err)
-
-
-@pytest.mark.parametrize("ta", [False, True])
-@pytest.mark.parametrize("tb", [False, True])
-def test_gemm_split_k(ta, tb, monkeypatch):
-    """96 long tiles on 74 clusters: the 2-SM kernel splits K in two halves (fp32 partials parked
-    by the first half, added by the second) — same result as the torch fp32 reference."""
-    from paper_2508_00960_b200 import kernels
-    monkeypatch.setenv("PPX_SPLITK", "1")
-    M, N, K = 2048, 3072, 8192
-    g = torch.Generator(device="cuda").manual_seed(5)
-    a = torch.randn((K, M) if ta else (M, K), device="cuda", generator=g).bfloat16()
-    b = torch.randn((N, K) if tb else (K, N), device="cuda", generator=g).bfloat16()
-    for _ in range(2):   # twice: the ready flags must reset themselves
-        out = kernels.gemm(a, b, ta, tb, out_dtype=torch.float32)
-        torch.cuda.synchronize()
-        ref = _ref(a, b, ta, tb)
-        err = ((out - ref).norm() / ref.norm()).item()
-        assert err < 1e-5, err
