@@ -295,6 +295,12 @@ typedef struct {
 } ppx_wgrad_item;
 ppx_status ppx_wgrad(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad_item* items, void* stream);
 
+/* phantom.py:210-267 as one launch: the weight gradients (+ fused update) of `nitems` items and the
+   error recurrence of the n ranks (io as for ppx_backward_delta_n), tiles scheduled longest-first
+   over the clusters.  The layer's reduced phantom gradient must already be in place. */
+ppx_status ppx_backward_fused(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad_item* items, int32_t n,
+                              const ppx_rank_io* io, int32_t B, ppx_act act_prev, void* stream);
+
 /* phantom.py:210-236 — delta_prev = (local^T delta + compressor^T r) * act'(pre_prev): ONE
    K-concatenated contraction [delta | r] . [L ; C]; `mask_src` is pre_prev or y_prev (only its
    sign is read; NULL for IDENTITY).  bias_grad_prev += sum_batch delta_prev if non-NULL. */

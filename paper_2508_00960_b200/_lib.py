@@ -107,6 +107,8 @@ _SIGS = {
     "ppx_error_phantoms_scatter": (_i32, [_vp, _i32, _i32, ctypes.POINTER(RankIO), _i32, _vp, ctypes.POINTER(Scatter),
                                            _vp]),
     "ppx_reduce_received": (_i32, [_vp, _i32, _i32, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "ppx_backward_fused": (_i32, [_vp, _i32, _i32, ctypes.POINTER(WgradItem), _i32, ctypes.POINTER(RankIO), _i32, _i32,
+                                   _vp]),
     "ppx_peer_push": (_i32, [_vp, _vp, _i64, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp]),
     "ppx_peer_signal": (_i32, [_vp, _i32, ctypes.POINTER(_vp), _vp, _vp]),
     "ppx_peer_wait": (_i32, [_vp, _i32, ctypes.POINTER(_vp), _vp, _vp, _vp]),

@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
       uint32_t phase = 0;
       unsigned long long st_empty = 0;
       const int epoch = P.epoch ? *(volatile int*)P.epoch : 0;
-      for (int t = t0; t < total; t += tstep) {
+      for (int i = 0, t; (t = tile_of(P, t0, tstep, i)) >= 0; ++i) {
         TileCoord tc = tile_coord<2 * BM>(P, t);
         const Problem& pr = P.probs[tc.prob];
         const int bnc = pr.BN / 2;
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
       int iter = 0;
       unsigned long long st_tempty = 0, st_full = 0;
       const unsigned long long c_start = kStats && P.stats ? clock64() : 0ull;
-      for (int t = t0; t < total; t += tstep, ++iter) {
+      for (int t; (t = tile_of(P, t0, tstep, iter)) >= 0; ++iter) {
         TileCoord tc = tile_coord<2 * BM>(P, t);
         const Problem& pr = P.probs[tc.prob];
         const int as = iter & 1;

@@ -55,7 +55,8 @@ constexpr int TMEM_COLS = 512;    // 2 accumulator stages x 256 fp32 columns
 constexpr int MAX_MAPS = 40;
 constexpr int MAX_PROBS = 16;
 constexpr int MAX_SEGS = 8;
-constexpr int MAX_REP = 7;         // peer replicas of an epilogue output (world <= 8)
+constexpr int MAX_REP = 7;
+constexpr int MAX_SCHED = 4096;    // tiles of one LPT-scheduled launch         // peer replicas of an epilogue output (world <= 8)
 constexpr int COLSUM_BYTES = 2 * BN_MAX * 4;     // per-CTA column-sum staging, double-buffered by tile parity
 constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 /*align*/ + 256 /*barriers*/ + COLSUM_BYTES;
 
@@ -146,6 +147,9 @@ struct alignas(64) GemmParams {
   int total_tiles;
   int dbg;             // debug: bit0 = skip the epilogue body (TMEM drain only by arrival)
   unsigned long long* stats;   // debug (PPX_DEBUG_STATS): per-role wait / busy clock sums, else null
+  int nsched;          // > 0: static LPT schedule — cluster c runs tiles sched[sched_off[c] .. sched_off[c+1])
+  uint16_t sched_off[76];
+  uint16_t sched[MAX_SCHED];
   int* epoch;          // launches with waiting problems: *epoch += 1 by the last CTA to exit
   unsigned int* done;  //   (CTA exit counter, self-resetting)
   int* bad;            //   |= 2 when a wait timed out
@@ -514,6 +518,16 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, int t) {
   return c;
 }
 
+// i-th tile of cluster (or CTA) c: the static LPT schedule when present, else round robin
+__device__ __forceinline__ int tile_of(const GemmParams& P, int c, int step, int i) {
+  if (P.nsched) {
+    const int b = P.sched_off[c] + i;
+    return b < P.sched_off[c + 1] ? (int)P.sched[b] : -1;
+  }
+  const int t = c + i * step;
+  return t < P.total_tiles ? t : -1;
+}
+
 // producer-side wait of a fused launch (see Problem::wait_ctr); TMA reads what the generic proxy
 // (local or NVLink stores) wrote, hence the proxy fence after the acquire
 // (bounded: after ~20 s it flags bit 1 of *P.bad and proceeds — a lost peer never hangs the GPU)
@@ -564,7 +578,7 @@ template <int MT>
 __device__ __forceinline__ void publisher_loop(const GemmParams& P, int t0, int tstep, uint32_t crank, int warp,
                                                int lane) {
   const int tid = (warp - W_PUB0) * 32 + lane;
-  for (int t = t0; t < P.total_tiles; t += tstep) {
+  for (int i = 0, t; (t = tile_of(P, t0, tstep, i)) >= 0; ++i) {
     TileCoord tc = tile_coord<MT>(P, t);
     const Problem& pr = P.probs[tc.prob];
     const Epilogue& E = pr.epi;
@@ -607,7 +621,7 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
   const int grp = warp >> 2;  // chunk parity drained by this warp
   unsigned long long st_wait = 0, st_busy = 0, st_tmem = 0, st_body = 0;
   int iter = 0;
-  for (int t = t0; t < total; t += tstep, ++iter) {
+  for (int t; (t = tile_of(P, t0, tstep, iter)) >= 0; ++iter) {
     TileCoord tc = tile_coord<MT>(P, t);
     const Problem& pr = P.probs[tc.prob];
     const Epilogue& E = pr.epi;

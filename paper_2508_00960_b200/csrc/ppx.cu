@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdarg>
 #include <cstdio>
@@ -169,6 +170,7 @@ struct Builder {
   bool want_pair = false, use_pair = false;
   int BKf = 64;   // K per stage of the kernel actually launched
   int fuse_world = 0;          // > 0: a fused compress + exchange + forward launch over this many GPUs
+  bool lpt = false;            // static longest-processing-time schedule of the tiles over the clusters
   int* fuse_epoch = nullptr;
   int* fuse_bad = nullptr;
   // MN-major A (activations / deltas of the weight-gradient GEMMs) as the interleaved 5D tile
@@ -626,7 +628,7 @@ struct Builder {
         if (!changed || t2 >= t1) { memcpy(P.probs, save, sizeof(Problem) * P.nprobs); break; }
       }
     }
-    if (use_pair && !getenv("PPX_NO_TAILSPLIT")) split_tail(ctx->num_sms / 2 - ctx->reserved_sms / 2);
+    if (use_pair && !lpt && !getenv("PPX_NO_TAILSPLIT")) split_tail(ctx->num_sms / 2 - ctx->reserved_sms / 2);
     for (int i = 0; i < P.nprobs && ok(); ++i)
       for (const PendingSeg& ps : pend[i]) finalize(&P.probs[i], ps);
     if (!ok()) return status;
@@ -637,6 +639,38 @@ struct Builder {
       tiles += ptiles(P.probs[i]);
     }
     P.total_tiles = tiles;
+    P.nsched = 0;
+    if (lpt && use_pair && !fuse_world && tiles <= ppx::MAX_SCHED && ctx->num_sms / 2 < 76) {
+      // LPT: tiles in decreasing cost (K stages + epilogue, scaled by tile width) each go to the
+      // least-loaded cluster; every role of a cluster walks the same list
+      const int sms_avail = ctx->num_sms - ctx->reserved_sms;
+      const int C = tiles < sms_avail / 2 ? tiles : sms_avail / 2;
+      std::vector<std::pair<double, int>> cost(tiles);
+      for (int i = 0; i < P.nprobs; ++i) {
+        const Problem& pr = P.probs[i];
+        int kst = 0;
+        for (int g = 0; g < pr.nsegs; ++g) kst += pr.segs[g].k_tiles;
+        const double c = (kst + 4.0) * pr.BN / 256.0;
+        for (int t = pr.tile_begin; t < pr.tile_begin + ptiles(pr); ++t) cost[t] = {-c, t};
+      }
+      std::stable_sort(cost.begin(), cost.end());
+      std::vector<double> load(C, 0.0);
+      std::vector<std::vector<int>> lists(C);
+      for (const auto& ct : cost) {
+        int best = 0;
+        for (int c = 1; c < C; ++c)
+          if (load[c] < load[best]) best = c;
+        load[best] -= ct.first;
+        lists[best].push_back(ct.second);
+      }
+      int o = 0;
+      for (int c = 0; c < C; ++c) {
+        P.sched_off[c] = (uint16_t)o;
+        for (int t : lists[c]) P.sched[o++] = (uint16_t)t;
+      }
+      P.sched_off[C] = (uint16_t)o;
+      P.nsched = tiles;
+    }
     if (fuse_world) {   // fused compress + exchange + forward: arrivals per epoch on this GPU
       if (!use_pair) return fail(ctx, PPX_E_CONFIG, "fused forward needs the 2-SM kernel (bf16, 64-aligned shapes)");
       int ct = 0;
@@ -1459,6 +1493,34 @@ ppx_status ppx_backward_delta_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx
     if (s != PPX_OK) return s;
   }
   return b.launch();
+}
+
+// Weight gradients (+ fused optimizer) of `nitems` items and the error recurrence of the n ranks as
+// ONE launch with a static LPT tile schedule: the long weight-gradient tiles and the short
+// recurrence tiles share the rounds (one logical rank per GPU leaves either launch alone at ~1.4
+// rounds of tiles).  Needs the reduced phantom gradient (r) of the layer already in place.
+ppx_status ppx_backward_fused(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad_item* items, int32_t n,
+                              const ppx_rank_io* io, int32_t B, ppx_act act_prev, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (nitems < 0 || (nitems > 0 && !items) || n < 0 || (n > 0 && !io))
+    return fail(ctx, PPX_E_CONFIG, "ppx_backward_fused: bad arguments");
+  Builder b(ctx, dt, stream);
+  for (int i = 0; i < nitems; ++i) {
+    ppx_status st = wgrad_add(ctx, dt, b, items[i]);
+    if (st != PPX_OK) return st;
+  }
+  for (int i = 0; i < n; ++i) {
+    ppx_status st = add_backward(ctx, dt, b, io[i], B, act_prev);
+    if (st != PPX_OK) return st;
+  }
+  b.lpt = getenv("PPX_NO_LPT") == nullptr;
+  ppx_status st = b.launch();
+  if (st != PPX_OK) return st;
+  for (int i = 0; i < nitems; ++i) {
+    st = wgrad_bias(ctx, dt, items[i], (cudaStream_t)stream);
+    if (st != PPX_OK) return st;
+  }
+  return PPX_OK;
 }
 
 ppx_status ppx_backward_delta(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, int32_t B, ppx_act act_prev,

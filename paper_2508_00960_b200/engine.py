@@ -146,6 +146,11 @@ class PhantomEngine:
         self.parity = 0
         # training steps skip the output layer's y store (PPX_STORE_OUTPUT=1 keeps it)
         self.skip_output = not os.environ.get("PPX_STORE_OUTPUT")
+        # weight gradients + error recurrence of a layer as one LPT-scheduled launch (after the
+        # reduce-scatter): default with one logical rank per GPU, where either launch alone leaves
+        # ~1.4 rounds of tiles (PPX_BWD_FUSED=1/0 forces it on / off)
+        bf = os.environ.get("PPX_BWD_FUSED", "")
+        self.bwd_fused = dtype == torch.bfloat16 and (bf == "1" or (bf == "" and self.R == 1 and world > 1))
         # timing experiments ONLY (wrong results): drop the backward reduce-scatter
         self._dbg_skip_rs = bool(os.environ.get("PPX_DEBUG_SKIP_RS"))
         self._dbg_skip_ag = bool(os.environ.get("PPX_DEBUG_SKIP_AG"))
@@ -342,7 +347,7 @@ class PhantomEngine:
     _KERNEL_CALLS = {"ppx_compress", "ppx_forward_update", "ppx_forward_output", "ppx_error_phantoms", "ppx_wgrad",
                      "ppx_backward_delta", "ppx_optimizer_step", "ppx_compress_n", "ppx_forward_n", "ppx_error_phantoms_n", "ppx_compress_push",
                      "ppx_peer_signal", "ppx_peer_wait", "ppx_peer_push", "ppx_forward_fused",
-                     "ppx_error_phantoms_scatter", "ppx_reduce_received",
+                     "ppx_error_phantoms_scatter", "ppx_reduce_received", "ppx_backward_fused",
                      "ppx_backward_delta_n"}
 
     def _call(self, name, *args):
@@ -502,6 +507,31 @@ class PhantomEngine:
                                                 None, self._received(l + 1, j), None,
                                                 ctypes.pointer(self._update(jj, l + 1, par))))
                 per_rank.append(items)
+            if self.bwd_fused and R * (4 if l < L - 1 else 3) <= 15:
+                # r_l first (exposed), then weight gradients + recurrence as ONE LPT-scheduled launch
+                if self.world > 1 and not nvrs:
+                    self._join(self.comm_stream, S)
+                if nvrs:
+                    own = self.H[l].data_ptr() + self.rank * R * slot * esz
+                    self._call("ppx_reduce_received", pdt, R, slot, self.world, self.rank, self._pbase + self._soff[l],
+                               own, self.Hr[l].data_ptr(), self._pbase + self._rcoff + 4 * l,
+                               self._rsepoch[l:].data_ptr(), self.bad.data_ptr(), st)
+                ios = []
+                if l > 0:
+                    for jj in range(R):
+                        j = self.local[jj]
+                        ios.append(self._io(jj, l, par, x=self.D[jj][cur].data_ptr(), ld_x=s,
+                                            out=self.D[jj][1 - cur].data_ptr(), ld_out=s,
+                                            mask=self.Y[par][jj][l].data_ptr() if self.act is Activation.RELU else None,
+                                            ld_m=s, received=self._received(l, j),
+                                            colsum=self.gbias[jj, l - 1].data_ptr()))
+                flat = [it for chunk in per_rank for it in chunk]
+                arr = (_lib.WgradItem * len(flat))(*flat)
+                self._keep.append(arr)
+                self._call("ppx_backward_fused", pdt, len(flat), arr, len(ios), self._ios(ios), B, self.act.code, st)
+                if l > 0:
+                    cur = 1 - cur
+                continue
             nprob = 2 + (1 if l < L - 1 else 0) if self.p > 1 else 1
             per = max(1, min(self.group, 16 // nprob))
             nl = -(-R // per)

@@ -136,3 +136,29 @@ def test_engine_pair_kernel_matches_oracle(graph):
     ref = _oracle_steps(model, x, y, L, 3, "sgd", lr)
     for a, b in zip(losses, ref):
         assert abs(a - b) <= 2e-2 * abs(b), (losses, ref)
+
+
+@pytest.mark.parametrize("p", [2, 4])
+@pytest.mark.parametrize("graph", [False, True])
+def test_engine_backward_fused_matches_oracle(graph, p, monkeypatch):
+    """PPX_BWD_FUSED=1: weight gradients (+ fused SGD) and the error recurrence of each layer as ONE
+    launch with a static longest-first tile schedule — bf16 steps against the float64 oracle."""
+    monkeypatch.setenv("PPX_BWD_FUSED", "1")
+    n, k, L, B, lr = 128 * p, 64, 3, 256, 3e-3
+    eng, model, x, y = _setup(n, p, k, L, B, torch.bfloat16, "sgd", lr)
+    assert eng.bwd_fused
+    if graph:
+        eng.capture()
+    losses = []
+    for _ in range(3):
+        eng.step(graph=graph)
+        losses.append(eng.read_loss())
+    ref = _oracle_steps(model, x, y, L, 3, "sgd", lr)
+    for a, b in zip(losses, ref):
+        assert abs(a - b) <= 2e-2 * abs(b), (losses, ref)
+    for jj in range(p):
+        for l in range(L):
+            v = eng.layer_views(jj, l)
+            assert nerr(v["local"], model[jj][l]["local"]) <= 2e-2
+            for i, d in v["decompressors"].items():
+                assert nerr(d, model[jj][l]["decompressors"][i]) <= 2e-2
