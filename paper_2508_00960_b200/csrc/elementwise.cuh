@@ -304,7 +304,6 @@ struct ReduceArgs {
   unsigned int* done;
 };
 __global__ void reduce_received_kernel(ReduceArgs a) {
-  __shared__ int ok;
   if (threadIdx.x == 0) {
     const int target = (int)((unsigned)(*(volatile int*)a.epoch + 1) * (unsigned)a.per_epoch);
     unsigned long long t0, t;
@@ -320,7 +319,6 @@ __global__ void reduce_received_kernel(ReduceArgs a) {
       }
       __nanosleep(64);
     }
-    ok = 1;
   }
   __syncthreads();
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -354,7 +352,6 @@ __global__ void reduce_received_kernel(ReduceArgs a) {
       atomicAdd(a.epoch, 1);
     }
   }
-  (void)ok;
 }
 inline cudaError_t launch_reduce_received(const ReduceArgs& a, cudaStream_t st) {
   long long blocks = (a.slot_x8 + 255) / 256;

@@ -104,7 +104,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
-  const int total = P.total_tiles;
   const int t0 = (int)(blockIdx.x >> 1);
   const int tstep = (int)(gridDim.x >> 1);
 

@@ -614,7 +614,6 @@ template <int MT, bool kPair>
 __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem_base, uint32_t tfull0,
                                               uint32_t tempty0, int t0, int tstep, uint32_t crank, int warp,
                                               int lane, float* cs_smem) {
-  const int total = P.total_tiles;
   auto tfull_bar = [&](int s) { return tfull0 + 8u * s; };
   auto tempty_bar = [&](int s) { return tempty0 + 8u * s; };
   const int wq = warp & 3;    // TMEM lane quadrant
