@@ -244,6 +244,22 @@ def make_data(eng, seed, cfg):
     return xs, ts
 
 
+def bind_to_gpu_cpus(gpu_index):
+    """Pin this rank to the host CPUs NVML reports as closest to its GPU, so the pinned host
+    batches of the e2e leg are first-touched on that GPU's NUMA node (PPX_NO_NUMA_BIND=1 skips)."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+        ncpu = os.cpu_count() or 1
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (ncpu + 63) // 64)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1 and 64 * i + b < ncpu}
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+    except Exception as exc:  # pragma: no cover - best effort, the bench runs unbound
+        print(f"[bench] cpu binding skipped: {exc}", file=sys.stderr)
+
+
 def run_tp(args, cfg, world, rank, local_rank, uid, eng, xs, barrier, dist):
     """The same-width Megatron tensor-parallel FFN (TPEngine) on the same GPUs, same batch."""
     import torch
@@ -346,6 +362,8 @@ def main():
     if world != args.gpus:
         world = args.gpus if world == 1 and args.gpus == 1 else world
     torch.cuda.set_device(local_rank)
+    if world > 1 and not os.environ.get("PPX_NO_NUMA_BIND"):
+        bind_to_gpu_cpus(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         uid = [_lib.Context.unique_id() if rank == 0 else None]
