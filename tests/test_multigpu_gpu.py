@@ -42,3 +42,20 @@ def test_engine_two_gpus_fused_forward(p, nvrs):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert '"pass": true' in r.stdout and '"fused": true' in r.stdout
+
+
+@pytest.mark.parametrize("p,n", [(4, 512), (8, 1024)])
+def test_engine_four_gpus_default_path(p, n):
+    """The default multi-GPU path on 4 GPUs (bf16, k = 64): fused compression + NVLink all-gather +
+    forward; p = 4 (one logical rank per GPU, the N = p shapes of the scaling run): NCCL
+    reduce-scatter + weight gradients and recurrence as one LPT-scheduled launch; p = 8 (two per
+    GPU): the NVLink reduce-scatter with 3 peers."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "4",
+           "--master-addr", "127.0.0.1", "--master-port", str(29540 + p), os.path.join(ROOT, "tools", "mp_parity.py"),
+           "--dtype", "bf16", "--p", str(p), "--width", str(n), "--k", "64", "--B", "256",
+           "--lr", "1e-4"]   # 3e-3 diverges at width 1024 in the oracle too (TrainingError, as the reference)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=dict(os.environ))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert '"pass": true' in r.stdout and '"fused": true' in r.stdout

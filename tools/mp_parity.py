@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--p", type=int, default=4)
     ap.add_argument("--k", type=int, default=32)
     ap.add_argument("--B", type=int, default=64)
+    ap.add_argument("--width", type=int, default=512)
+    ap.add_argument("--lr", type=float, default=3e-3)
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -29,7 +31,7 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     uid = [_lib.Context.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
-    n, p, k, L, B, lr = 512, args.p, args.k, 3, args.B, 3e-3
+    n, p, k, L, B, lr = args.width, args.p, args.k, 3, args.B, args.lr
     dtype = torch.float32 if args.dtype == "fp32" else torch.bfloat16
     tol = 1e-4 if args.dtype == "fp32" else 2e-2
     model = po.init_phantom_model(n, p, k, L, 3)
