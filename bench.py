@@ -1,24 +1,40 @@
 #!/usr/bin/env python
 """Phantom-parallel FFN training throughput on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config c3]
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config c3|c2|c4|c5]
 
 Workload (config C3, the north_star's headline): width n=16384, 8 layers, p=8 logical phantom
 ranks, k=128, batch 8192, bf16, ReLU, mean half-squared loss, SGD — the SAME model at every N
-(strong scaling): N GPUs each own 8/N logical ranks (N=1 runs all 8 on one GPU, the phantom
-all-gather / reduce-scatter then stay in HBM; N>1 adds NCCL over NVLink).  One step = one
-pp_iteration + optimizer update over one batch of synthetic teacher data (training.py:181-213,
-276-309).  Timed with CUDA events over K CUDA-graph replays, max over ranks.
+(strong scaling): N GPUs each own 8/N logical ranks (N=1 runs all 8 on one GPU and the phantom
+all-gather / reduce-scatter stay in HBM; N>1 exchanges phantoms over NVLink inside our kernels).
+One step = one pp_iteration + optimizer update over one batch of synthetic teacher data
+(reference training.py:181-213, 276-309).  Timed with CUDA events over K CUDA-graph replays,
+max over ranks.  The same JSON line also carries:
 
---impl reference times the reference algorithm's CPU implementation (the numpy oracle port,
-oracle/phantom_oracle.py; the reference itself is pure Python and is not present on the GPU box)
-on this box's host cores on a bounded sample of the same workload.
+  roofline    the step's per-kernel table (CUDA events around every launch of an eager step,
+              each launch tagged with its algorithmic GEMM FLOPs) and the dominant kernel (largest
+              time share) against the measured bf16 peak; `traffic` = that kernel's DRAM bytes
+              per launch from the committed ncu capture (profiles/traffic.json, commit-stamped)
+  r1_shapes   (N=1) the same step with one logical rank per launch: the per-GPU kernels of the
+              8-GPU run, so every 1-GPU bench records their efficiency
+  inference   (C3/C5) forward-only samples/s of the same model (config C5 at k = 128)
+  energy      NVML joules per epoch (64 batches) over >= --energy-seconds of steady-state steps
+  tp          the same-width Megatron tensor-parallel pipeline on the same GPUs (its energy too)
+  e2e         the public API with pinned HOST batches: H2D of inputs+targets and D2H of the loss
+              inside the timed region
+  cpu_baseline  the reference algorithm on this box's host cores (bounded sample)
+
+--config c5 runs the inference sweep (k = 32..512) instead of training.  --impl reference times
+the UNMODIFIED reference (phantomsim, installed into baseline/_ref from /root/reference) on the
+host cores through its own API (Communicator threads + pp_iteration + sgd_step); if that install
+is absent it falls back to the pinned oracle port (kind "port").
 """
 
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -31,10 +47,13 @@ sys.path.insert(0, ROOT)
 
 METRIC = "FFN train samples/s @1/2/4/8 B200, % TC roofline, J/epoch vs tensor-parallel"
 CONFIGS = {
-    "c3": dict(n=16384, p=8, k=128, layers=8, batch=8192),
-    "c2": dict(n=8192, p=4, k=64, layers=8, batch=8192),
     "c1": dict(n=1024, p=2, k=16, layers=4, batch=64),
+    "c2": dict(n=8192, p=4, k=64, layers=8, batch=8192),
+    "c3": dict(n=16384, p=8, k=128, layers=8, batch=8192),
+    "c4": dict(n=65536, p=8, k=256, layers=16, batch=8192),
+    "c5": dict(n=16384, p=8, k=128, layers=8, batch=8192),
 }
+C5_KS = (32, 64, 128, 256, 512)
 STEPS_PER_EPOCH = 64      # epoch = 64 * B samples
 
 
@@ -47,28 +66,31 @@ def peaks():
         return 1590.0, 1400.0, 6650.0, "fallback"
 
 
+def refuse_debug_knobs():
+    bad = sorted(k for k in os.environ if k.startswith("PPX_DEBUG"))
+    if bad:
+        sys.exit(f"bench.py: refusing to run with debug knobs set ({', '.join(bad)}): they change results")
+
+
 # ---------------------------------------------------------------------------------------------
 # clocks / energy
 # ---------------------------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """NVML polling thread (5 ms period) over the timed region: SM clock + throttle reasons."""
 
-    def __init__(self, gpu_index: int):
-        self.idx = gpu_index
-        self.proc = None
-        self.lines = []
+    def __init__(self, cuda_index: int):
+        self.idx = cuda_index
+        self.ok = False
+        self.sm, self.smax, self.reasons = [], None, set()
 
     def start(self):
-        """NVML polling thread (5 ms period) over the timed region; nvidia-smi -lms as fallback."""
         try:
             import pynvml
-            pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            from paper_2508_00960_b200.energy import nvml_handle
+            h = nvml_handle(self.idx)
             get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
                 pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
-            smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.smax = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
             bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                     "sw_power_cap": 0x4}
             self._stop = threading.Event()
@@ -76,101 +98,96 @@ class ClockSampler:
             def poll():
                 while not self._stop.is_set():
                     try:
-                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
                         r = get_reasons(h)
-                        act = ["Active" if r & b else "Not Active" for b in
-                               (bits["hw_slowdown"], bits["hw_thermal_slowdown"], bits["sw_thermal_slowdown"],
-                                bits["sw_power_cap"])]
-                        self.lines.append(", ".join([str(self.idx), str(sm), str(smax), "0", hex(r)] + act))
+                        self.reasons.update(nm for nm, b in bits.items() if r & b)
                     except Exception:
                         pass
                     self._stop.wait(0.005)
             self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
-            self.proc = "nvml"
-            return
-        except Exception:
-            self.proc = None
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "50"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.ok = True
+        except Exception as exc:  # pragma: no cover
+            self.err = str(exc)
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        if self.proc == "nvml":
-            self._stop.set()
-            self.t.join(timeout=1)
-        else:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                smax = float(parts[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        self._stop.set()
+        self.t.join(timeout=1)
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.smax,
+                "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
-def energy_mj(gpu_index):
+def energy_mj(cuda_index):
+    from paper_2508_00960_b200.energy import energy_mj as e
+    return e(cuda_index)
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU baseline / reference arm
+# ---------------------------------------------------------------------------------------------
+def _phantomsim():
+    """The unmodified reference package from baseline/_ref (None if it was not installed)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "phantomsim")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
     try:
-        import pynvml
-        pynvml.nvmlInit()
-        h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
-        return float(pynvml.nvmlDeviceGetTotalEnergyConsumption(h))
+        import phantomsim
+        return phantomsim
     except Exception:
         return None
 
 
-# ---------------------------------------------------------------------------------------------
-# CPU baseline / reference arm (oracle port)
-# ---------------------------------------------------------------------------------------------
-def cpu_sample(n, p, k, layers, batch, iters=2):
-    """Time the oracle's pp_iteration (reference algorithm, float64 numpy/OpenBLAS) on the host."""
+def reference_steps(n, p, k, layers, batch, steps, warmup):
+    """Time `steps` training iterations of the reference's own CPU implementation: phantomsim's
+    Communicator (one thread per rank) running pp_iteration + sgd_step (training.py:276-303) on a
+    random model of the configured shape.  Falls back to the pinned oracle port.  Returns
+    (seconds per step, kind, threads used)."""
     import numpy as np
-    from oracle import phantom_oracle as po
+    ps = _phantomsim()
+    cores = os.cpu_count() or 1
     s = n // p
     rng = np.random.default_rng(0)
-    model = []
-    for j in range(p):
-        row = []
-        for _ in range(layers):
-            a = (6.0 / (2 * s)) ** 0.5
-            row.append({"local": rng.uniform(-a, a, (s, s)), "compressor": rng.uniform(-a, a, (k, s)),
-                        "decompressors": {i: rng.uniform(-a, a, (s, k)) for i in range(p) if i != j},
-                        "bias": np.zeros(s)})
-        model.append(row)
-    x = [rng.standard_normal((s, batch)) for _ in range(p)]
-    y = [np.maximum(rng.standard_normal((s, batch)), 0) for _ in range(p)]
-    po.pp_iteration(model, ["relu"] * layers, x, y, "mean")   # warm-up
-    times = []
-    for _ in range(iters):
+    a = (6.0 / (2 * s)) ** 0.5
+    xs = [rng.standard_normal((s, batch)) for _ in range(p)]
+    ys = [np.maximum(rng.standard_normal((s, batch)), 0) for _ in range(p)]
+    if ps is not None:
+        acts = [ps.Activation.RELU] * layers
+        model = [[ps.PhantomLayer(local=rng.uniform(-a, a, (s, s)), compressor=rng.uniform(-a, a, (k, s)),
+                                  decompressors={i: rng.uniform(-a, a, (s, k)) for i in range(p) if i != j},
+                                  bias=np.zeros(s)) for _ in range(layers)] for j in range(p)]
+        from phantomsim.training import _pp_param_lists
+
+        def worker(comm, rank, nsteps):
+            for _ in range(nsteps):
+                out = ps.pp_iteration(comm, rank, model[rank], acts, xs[rank], ys[rank], "mean")
+                params, grads, names = _pp_param_lists(model[rank], out.grads)
+                ps.sgd_step(params, grads, 1e-4, names=names)
+        comm = ps.Communicator(p, mode="threads", timeout=3600.0)
+        if warmup:
+            comm.run(worker, warmup)
         t0 = time.perf_counter()
-        po.pp_iteration(model, ["relu"] * layers, x, y, "mean")
-        times.append(time.perf_counter() - t0)
-    return min(times)
+        comm.run(worker, steps)
+        return (time.perf_counter() - t0) / steps, "reference", cores
+    from oracle import phantom_oracle as po
+    model = [[{"local": rng.uniform(-a, a, (s, s)), "compressor": rng.uniform(-a, a, (k, s)),
+               "decompressors": {i: rng.uniform(-a, a, (s, k)) for i in range(p) if i != j}, "bias": np.zeros(s)}
+              for _ in range(layers)] for j in range(p)]
+
+    def one():
+        out = po.pp_iteration(model, ["relu"] * layers, xs, ys, "mean")
+        for j in range(p):
+            params, gs = po.pp_param_list(model[j], out["grads"][j])
+            po.sgd_step(params, gs, 1e-4)
+    for _ in range(warmup):
+        one()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    return (time.perf_counter() - t0) / steps, "port", cores
 
 
 def run_reference(args, cfg):
@@ -179,40 +196,42 @@ def run_reference(args, cfg):
         return 0
     cores = os.cpu_count() or 1
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
-    sample_b = 256
     n, p, k, L = cfg["n"], cfg["p"], cfg["k"], cfg["layers"]
-    import numpy as np
-    from oracle import phantom_oracle as po
-    s = n // p
-    rng = np.random.default_rng(0)
-    a = (6.0 / (2 * s)) ** 0.5
-    model = [[{"local": rng.uniform(-a, a, (s, s)), "compressor": rng.uniform(-a, a, (k, s)),
-               "decompressors": {i: rng.uniform(-a, a, (s, k)) for i in range(p) if i != j}, "bias": np.zeros(s)}
-              for _ in range(L)] for j in range(p)]
-    x = [rng.standard_normal((s, sample_b)) for _ in range(p)]
-    y = [np.maximum(rng.standard_normal((s, sample_b)), 0) for _ in range(p)]
-    for _ in range(args.warmup):
-        po.pp_iteration(model, ["relu"] * L, x, y, "mean")
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        out = po.pp_iteration(model, ["relu"] * L, x, y, "mean")
-        for j in range(p):
-            params, gs = po.pp_param_list(model[j], out["grads"][j])
-            po.sgd_step(params, gs, 1e-4)
-    dt = (time.perf_counter() - t0) / args.steps
+    sample_b = 256
+    sample_l = L if n <= 16384 else 1   # C4's float64 weights do not fit host RAM: one layer, x L
+    dt, kind, threads = reference_steps(n, p, k, sample_l, sample_b, args.steps, min(args.warmup, 1))
+    dt *= L / sample_l
     v = sample_b / dt
-    sample = (f"full {args.config} model (n={n}, p={p}, k={k}, L={L}) float64 pp_iteration+SGD at batch "
-              f"{sample_b} per step (samples/s is linear in batch for this GEMM-bound path)")
+    what = "phantomsim (unmodified reference, baseline/_ref)" if kind == "reference" else "oracle port of phantomsim"
+    sample = (f"{what}: Communicator(p={p}, threads) pp_iteration + sgd_step, float64, {args.config} model "
+              f"(n={n}, p={p}, k={k}, L={sample_l}{f' scaled x{L}' if sample_l != L else ''}) at batch {sample_b} "
+              f"per step (samples/s is linear in batch for this GEMM-bound path)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"phantom FFN {args.config}: n={n}, L={L}, p={p}, k={k}, batch {sample_b} (CPU sample)",
                    "global_batch": sample_b, "parallelism": f"pp{p} simulated in one process"},
-        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
     return 0
+
+
+def cpu_baseline(args, cfg):
+    """The reference on this box's host cores, one layer of the model at batch 256, scaled to L."""
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
+    n, p, k, L = cfg["n"], cfg["p"], cfg["k"], cfg["layers"]
+    sample_b = 256
+    try:
+        dt, kind, threads = reference_steps(n, p, k, 1, sample_b, 2, 1)
+        return {"value": sample_b / (dt * L), "unit": "samples/s", "cores": threads, "kind": kind,
+                "sample": f"{'phantomsim' if kind == 'reference' else 'oracle port'} pp_iteration + sgd_step "
+                          f"(float64, numpy/OpenBLAS, {threads} threads) of ONE layer of the {args.config} model "
+                          f"(all {p} ranks) at batch {sample_b}, mean of 2 after 1 warm-up, scaled x{L} layers"}
+    except Exception as exc:  # pragma: no cover
+        return {"value": None, "unit": "samples/s", "cores": cores, "kind": "reference", "sample": f"failed: {exc}"}
 
 
 # ---------------------------------------------------------------------------------------------
@@ -244,13 +263,13 @@ def make_data(eng, seed, cfg):
     return xs, ts
 
 
-def bind_to_gpu_cpus(gpu_index):
+def bind_to_gpu_cpus(cuda_index):
     """Pin this rank to the host CPUs NVML reports as closest to its GPU, so the pinned host
     batches of the e2e leg are first-touched on that GPU's NUMA node (PPX_NO_NUMA_BIND=1 skips)."""
     try:
         import pynvml
-        pynvml.nvmlInit()
-        h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+        from paper_2508_00960_b200.energy import nvml_handle
+        h = nvml_handle(cuda_index)
         ncpu = os.cpu_count() or 1
         words = pynvml.nvmlDeviceGetCpuAffinity(h, (ncpu + 63) // 64)
         cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1 and 64 * i + b < ncpu}
@@ -260,75 +279,98 @@ def bind_to_gpu_cpus(gpu_index):
         print(f"[bench] cpu binding skipped: {exc}", file=sys.stderr)
 
 
-def run_tp(args, cfg, world, rank, local_rank, uid, eng, xs, barrier, dist):
-    """The same-width Megatron tensor-parallel FFN (TPEngine) on the same GPUs, same batch."""
+class Dist:
+    def __init__(self, world, rank, local_rank):
+        self.world, self.rank, self.local = world, rank, local_rank
+        if world > 1:
+            import torch.distributed as dist
+            self.dist = dist
+
+    def barrier(self):
+        # drain our own NCCL work first: two communicators' kernels must never interleave
+        import torch
+        torch.cuda.synchronize()
+        if self.world > 1:
+            self.dist.barrier()
+        torch.cuda.synchronize()
+
+    def reduce(self, vals, op="max"):
+        import torch
+        t = torch.tensor(vals, device="cuda", dtype=torch.float64)
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM)
+        return [float(v) for v in t.tolist()]
+
+    def uid(self):
+        from paper_2508_00960_b200 import _lib
+        if self.world == 1:
+            return None
+        u = [_lib.Context.unique_id() if self.rank == 0 else None]
+        self.dist.broadcast_object_list(u, src=0)
+        return u[0]
+
+
+def timed_steps(eng, D, steps, graph=True):
+    """ms per step (CUDA events on the launching stream, max over ranks)."""
     import torch
-    from paper_2508_00960_b200 import _lib, kernels
-    from paper_2508_00960_b200.schedule import tp_comm_bytes_per_step
-    from paper_2508_00960_b200.tensor_parallel import TPEngine, tp_step_flops
-    n, L, B = cfg["n"], cfg["layers"], cfg["batch"]
-    # full replicated input / teacher targets of the dense-width task
-    g = torch.Generator(device=eng.dev)
-    g.manual_seed(1234)
-    X = torch.randn((B, n), generator=g, device=eng.dev).to(torch.bfloat16)
-    Xr = torch.empty_like(X)
-    eng.ctx.call("ppx_bias_act", eng.pdt, B, n, X.data_ptr(), n, None, 0, Xr.data_ptr(), n,
-                 torch.cuda.current_stream().cuda_stream)
-    gt = torch.Generator(device=eng.dev)
-    gt.manual_seed(99)
-    W = (torch.randn((n, n), generator=gt, device=eng.dev) / n ** 0.5).to(torch.bfloat16)
-    T = kernels.gemm(Xr, W, transpose_b=True, out_dtype=torch.bfloat16, relu=True, ctx=eng.ctx)
-    del W, Xr
-    eng.close()                      # free the phantom engine's graphs + communicator first
-    torch.cuda.empty_cache()
-    tpe = TPEngine(n, L, B, world=world, rank=rank, device=local_rank,
-                   uid=uid if world == 1 else _shared_uid(rank, world, dist), lr=3e-6, dtype=torch.bfloat16)
-    tpe.set_batch(X, T, 0)
-    tpe.set_batch(X, T, 1)
-    del X, T
-    tpe.step(graph=False)
-    tpe.read_loss()
-    tpe.capture()
-    for _ in range(2):
-        tpe.step()
-    tpe.read_loss()
-    barrier()
-    e0 = energy_mj(local_rank)
     S = torch.cuda.current_stream()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    steps = max(3, min(args.steps, 10))
-    ev0.record(S)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    D.barrier()
+    e0.record(S)
     for _ in range(steps):
-        tpe.step()
-    ev1.record(S)
-    barrier()
-    e1 = energy_mj(local_rank)
-    t = torch.tensor([ev0.elapsed_time(ev1) / steps], device="cuda")
-    j = torch.tensor([((e1 - e0) / 1e3 / steps) if (e0 is not None and e1 is not None) else float("nan")],
-                     device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(j, op=dist.ReduceOp.SUM)
-    ms = float(t.item())
-    loss = tpe.read_loss()
-    flops = tp_step_flops(n, world, L, B)
-    out = {"pipeline": f"Megatron tensor-parallel FFN n={n}, L={L}, batch {B}, column/row pairs, "
-                       f"{world} GPU(s), same kernels, SGD fused", "value": B / (ms / 1e3), "unit": "samples/s",
-           "ms_per_step": ms, "steps": steps, "step_tflops_per_gpu": flops / (ms / 1e3) / 1e12,
-           "j_per_step_all_gpus": float(j.item()), "j_per_epoch": float(j.item()) * STEPS_PER_EPOCH,
-           "comm_bytes_per_step_per_gpu": tp_comm_bytes_per_step(n, L, B, world), "loss": loss,
-           "gpu_launches": tpe.launch_count * steps}
-    if world > 1:
-        barrier()
-    tpe.close()
-    return out
+        eng.step(graph=graph)
+    e1.record(S)
+    D.barrier()
+    return D.reduce([e0.elapsed_time(e1) / steps])[0]
 
 
-def _shared_uid(rank, world, dist):
-    from paper_2508_00960_b200 import _lib
-    uid = [_lib.Context.unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
-    return uid[0]
+def energy_window(eng, D, ms_per_step, seconds, step=None):
+    """NVML joules per step over >= `seconds` of steady-state graph replays (all GPUs summed)."""
+    import math as _m
+    step = step or (lambda: eng.step())
+    steps = max(3, int(_m.ceil(seconds * 1e3 / max(ms_per_step, 1e-3))))
+    D.barrier()
+    t0 = time.perf_counter()
+    e0 = energy_mj(D.local)
+    for i in range(steps):
+        step()
+        if i % 64 == 63:
+            import torch
+            torch.cuda.synchronize()
+    D.barrier()
+    e1 = energy_mj(D.local)
+    wall = time.perf_counter() - t0
+    j = ((e1 - e0) / 1e3 / steps) if (e0 is not None and e1 is not None) else float("nan")
+    j_all = D.reduce([j], op="sum")[0]
+    return {"j_per_step_all_gpus": j_all, "j_per_epoch": j_all * STEPS_PER_EPOCH,
+            "epoch_samples": STEPS_PER_EPOCH * eng.B, "window_s": wall, "window_steps": steps}
+
+
+def kernel_table(seq, peak, steps=1):
+    """Aggregate profile_step output [(call, ms, flops)] -> per-kind rows + dominant kind."""
+    rows = {}
+    for name, ms, fl in seq:
+        r = rows.setdefault(name, {"launches": 0, "ms": 0.0, "flops": 0})
+        r["launches"] += 1
+        r["ms"] += ms
+        r["flops"] += fl
+    total = sum(r["ms"] for r in rows.values()) or 1.0
+    out = {}
+    for name, r in sorted(rows.items(), key=lambda kv: -kv[1]["ms"]):
+        tf = r["flops"] / (r["ms"] / 1e3) / 1e12 if r["ms"] > 0 and r["flops"] else None
+        out[name] = {"launches_per_step": r["launches"] // steps, "ms_per_step": r["ms"] / steps,
+                     "share": r["ms"] / total, "flops_per_launch": r["flops"] // max(r["launches"], 1),
+                     "ms_per_launch": r["ms"] / max(r["launches"], 1),
+                     "tflops": tf, "frac_of_burst": (tf / peak) if tf else None}
+    return out, total / steps
+
+
+def profile(eng, D, reps=3):
+    seq = []
+    for _ in range(reps):
+        seq += eng.profile_step()
+    D.barrier()
+    return seq
 
 
 def main():
@@ -339,11 +381,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--optimizer", default="sgd", choices=["sgd", "adam"])
+    ap.add_argument("--energy-seconds", type=float, default=20.0)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tp", action="store_true")
+    ap.add_argument("--no-r1", action="store_true")
     args = ap.parse_args()
+    refuse_debug_knobs()
     cfg = dict(CONFIGS[args.config])
     if args.batch:
         cfg["batch"] = args.batch
@@ -351,40 +397,31 @@ def main():
         return run_reference(args, cfg)
 
     import torch
-    import torch.distributed as dist
-    from paper_2508_00960_b200 import _lib
     from paper_2508_00960_b200.engine import PhantomEngine, pp_step_flops
     from paper_2508_00960_b200.schedule import comm_bytes_per_step
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        world = args.gpus if world == 1 and args.gpus == 1 else world
     torch.cuda.set_device(local_rank)
     if world > 1 and not os.environ.get("PPX_NO_NUMA_BIND"):
         bind_to_gpu_cpus(local_rank)
     if world > 1:
+        import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        uid = [_lib.Context.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        uid = uid[0]
-    else:
-        uid = None
+    D = Dist(world, rank, local_rank)
+    uid = D.uid()
     n, p, k, L, B = cfg["n"], cfg["p"], cfg["k"], cfg["layers"], cfg["batch"]
+    peak, peak_sus, hbm, peak_kind = peaks()
+    use_graph = not args.no_graph
+    if args.config == "c5":
+        return run_inference_sweep(args, cfg, D, uid, peak)
+
     eng = PhantomEngine(n, p, k, L, B, world=world, rank=rank, device=local_rank, uid=uid,
-                        optimizer="sgd", lr=3e-6, dtype=torch.bfloat16)
+                        optimizer=args.optimizer, lr=3e-6, dtype=torch.bfloat16)
     xs, ts = make_data(eng, 1234, cfg)
     eng.set_batch(xs, ts, 0)
     eng.set_batch(xs, ts, 1)
-    use_graph = not args.no_graph
-
-    def barrier():
-        # drain our own NCCL work first: two communicators' kernels must never interleave
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
 
     # warm-up: eager step (sets kernel attributes), capture, graph replays
     eng.step(graph=False)
@@ -394,124 +431,61 @@ def main():
     for _ in range(max(args.warmup - 1, 2)):
         eng.step(graph=use_graph)
     loss0 = eng.read_loss()
-    barrier()
 
-    dev_index = local_rank
-    sampler = ClockSampler(dev_index)
+    sampler = ClockSampler(local_rank)
     sampler.start()
-    e0 = energy_mj(dev_index)
-    S = torch.cuda.current_stream()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    ev0.record(S)
-    for _ in range(args.steps):
-        eng.step(graph=use_graph)
-    ev1.record(S)
-    barrier()
-    e1 = energy_mj(dev_index)
+    ms = timed_steps(eng, D, args.steps, use_graph)
     clocks = sampler.stop()
-    t_local = ev0.elapsed_time(ev1) / args.steps   # ms per step
     loss1 = eng.read_loss()
-
-    t = torch.tensor([t_local], device="cuda")
-    joules = torch.tensor([((e1 - e0) / 1e3 / args.steps) if (e0 is not None and e1 is not None) else float("nan")],
-                          device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(joules, op=dist.ReduceOp.SUM)
-    ms = float(t.item())
-    j_step = float(joules.item())
     value = B / (ms / 1e3)
-
-    # ---- dominant-kernel probe: the fused forward GEMM (local + decompress, bias+ReLU epilogue)
-    peak, peak_sus, hbm, peak_kind = peaks()
-    lmid = L // 2
-    probe_iters = 20
-    pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    import ctypes
-    lay = eng._layer(0, lmid, eng.parity)
-    y = eng.Y[eng.parity][0][lmid]
-    out = eng.Y[eng.parity][0][lmid + 1]
-    def k1():
-        eng.ctx.call("ppx_forward_update", eng.pdt, ctypes.byref(lay), B, eng.act.code, y.data_ptr(), eng.s,
-                     eng.G[lmid].data_ptr(), out.data_ptr(), eng.s, None, 0, torch.cuda.current_stream().cuda_stream)
-    for _ in range(3):
-        k1()
-    # replay the launches from a CUDA graph so host launch cost never gates the GPU
-    pg = torch.cuda.CUDAGraph()
-    cs = torch.cuda.Stream()
-    cs.wait_stream(S)
-    with torch.cuda.graph(pg, stream=cs):
-        for _ in range(probe_iters):
-            k1()
-    pg.replay()
-    torch.cuda.synchronize()
-    pe0.record(S)
-    pg.replay()
-    pe1.record(S)
-    torch.cuda.synchronize()
-    k1_ms = pe0.elapsed_time(pe1) / probe_iters
-    s = n // p
-    k1_flops = 2 * B * s * (s + (p - 1) * k)
-    k1_tflops = k1_flops / (k1_ms / 1e3) / 1e12
     step_flops = eng.R * pp_step_flops(n, p, k, L, B)
     step_tflops = step_flops / (ms / 1e3) / 1e12
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "k1_traffic.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+
+    # ---- per-kernel roofline of the step: CUDA events around every launch of eager steps
+    seq = profile(eng, D)
+    kernels, kern_ms = kernel_table(seq, peak, steps=3)
+    dom_name, dom = next(iter(kernels.items()))
+    flops_check = sum(f for _, _, f in seq) / 3
+    traffic = stamped_traffic(dom_name)
+    roofline = {"bound": "tensor", "kernel": dom_name, "achieved": dom["tflops"], "peak": peak, "unit": "TFLOP/s",
+                "frac": dom["tflops"] / peak, "traffic": traffic.get("dram_bytes_per_launch"),
+                "traffic_source": traffic.get("source"), "flops_per_launch": dom["flops_per_launch"],
+                "ms_per_launch": dom["ms_per_launch"], "peak_kind": f"{peak_kind} burst",
+                "step_tflops_per_gpu": step_tflops, "step_frac_of_sustained": step_tflops / peak_sus,
+                "step_frac_of_burst": step_tflops / peak, "kernel_sum_ms_per_step": kern_ms,
+                "kernel_sum_frac_of_burst": step_flops / (kern_ms / 1e3) / 1e12 / peak,
+                "flops_tagged_per_step": flops_check, "flops_algorithmic_per_step": step_flops,
+                "kernels": kernels}
+
+    # ---- inference (config C5 at this k): forward-only graph replays of the same model
+    inference = None
+    if args.config in ("c3", "c2"):
+        inference = time_inference(eng, D, args.steps, use_graph, peak)
+
+    # ---- NVML energy over >= energy_seconds of steady-state training steps
+    energy = energy_window(eng, D, ms, args.energy_seconds, step=lambda: eng.step(graph=use_graph))
 
     # ---- end-to-end through the public API: pinned host batches, H2D + D2H(loss) in the timed region
-    e2e = None
-    if not args.no_e2e:
-        xh = torch.stack([x.cpu() for x in xs]).pin_memory()
-        th = torch.stack([t_.cpu() for t_ in ts]).pin_memory()
-        h2d = 2 * xh.numel() * xh.element_size()
-        barrier()
-        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        q0.record(S)
-        ready = eng.load_batch_async(xh, th, eng.parity)
-        prev_done = None
-        for i in range(args.steps):
-            S.wait_event(ready)
-            par = eng.parity
-            eng.step(graph=use_graph)
-            done = torch.cuda.Event()
-            done.record(S)
-            if i + 1 < args.steps:
-                # the next batch goes into the other parity's buffers, last read by step i-1:
-                # its H2D overlaps step i
-                if prev_done is not None:
-                    eng.copy_stream.wait_event(prev_done)
-                ready = eng.load_batch_async(xh, th, 1 - par)
-            prev_done = done
-            eng.read_loss()                              # D2H of the step's loss (+ non-finite flag)
-        q1.record(S)
-        barrier()
-        te = torch.tensor([q0.elapsed_time(q1) / args.steps], device="cuda")
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": B / (float(te.item()) / 1e3), "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": 8}
+    e2e = None if args.no_e2e else time_e2e(eng, D, xs, ts, args.steps, use_graph, B)
+
+    r1 = None
+    if world == 1 and p > 1 and not args.no_r1 and args.config in ("c3", "c2"):
+        eng.close()
+        del eng
+        torch.cuda.empty_cache()
+        r1 = time_r1_shapes(cfg, D, xs, ts, args, peak, peak_sus)
+        eng = None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cores = os.cpu_count() or 1
-        sample_b, sample_l = 256, 1
-        try:
-            tcpu = cpu_sample(n, p, k, sample_l, sample_b)
-            cpu = {"value": sample_b / (tcpu * L / sample_l), "unit": "samples/s", "cores": cores, "kind": "port",
-                   "sample": f"oracle pp_iteration (float64, numpy/OpenBLAS) of ONE layer of the {args.config} model "
-                             f"(all {p} ranks) at batch {sample_b}, best of 2, scaled x{L // sample_l} layers"}
-        except Exception as exc:  # pragma: no cover
-            cpu = {"value": None, "unit": "samples/s", "cores": cores, "kind": "port", "sample": f"failed: {exc}"}
+        cpu = cpu_baseline(args, cfg)
 
     tp = None
-    if not args.no_tp and L % 2 == 0:
-        tp = run_tp(args, cfg, world, rank, local_rank, uid, eng, xs, barrier, dist)
+    if not args.no_tp and L % 2 == 0 and args.config != "c4":
+        tp = run_tp(args, cfg, D, eng, uid)
+    elif eng is not None:
+        D.barrier()
+        eng.close()
 
     if rank == 0:
         line = {
@@ -519,42 +493,227 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"phantom FFN {args.config}: n={n}, L={L}, p={p} logical ranks, k={k}, "
-                                   f"batch {B}, ReLU, mean loss, SGD; {eng.R} logical rank(s) per GPU",
+                                   f"batch {B}, ReLU, mean loss, {args.optimizer.upper()}; "
+                                   f"{p // world} logical rank(s) per GPU",
                        "global_batch": B, "width": n, "layers": L, "p": p, "k": k,
                        "parallelism": f"phantom pp{p} over {world} GPU(s)",
                        "l2": "working set per step (weights + activations) exceeds the 126 MB L2; no flush",
                        "graphs": use_graph},
-            "roofline": {"bound": "tensor", "achieved": k1_tflops, "peak": peak, "unit": "TFLOP/s",
-                         "frac": k1_tflops / peak, "traffic": traffic, "kernel": "fused forward GEMM (ppx_forward_update)",
-                         "flops_per_launch": k1_flops, "ms_per_launch": k1_ms, "peak_kind": f"{peak_kind} burst",
-                         "step_tflops_per_gpu": step_tflops, "step_frac_of_sustained": step_tflops / peak_sus},
+            "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
-            "energy": {"j_per_step_all_gpus": j_step, "j_per_epoch": j_step * STEPS_PER_EPOCH,
-                       "epoch_samples": STEPS_PER_EPOCH * B},
+            "energy": energy,
             "loss": {"after_warmup": loss0, "after_timed": loss1},
             "comm_bytes_per_step_per_gpu": comm_bytes_per_step(n, p, k, L, B, world),
+            "r1_shapes": r1,
+            "inference": inference,
             "tp": tp,
         }
         if tp and tp.get("value"):
             line["pp_vs_tp"] = {"speedup": value / tp["value"],
                                 "comm_bytes_ratio": (line["comm_bytes_per_step_per_gpu"] / tp["comm_bytes_per_step_per_gpu"]
                                                      if tp["comm_bytes_per_step_per_gpu"] else None),
-                                "energy_per_epoch_ratio": (j_step / tp["j_per_step_all_gpus"]
-                                                           if tp.get("j_per_step_all_gpus") else None)}
+                                "energy_per_epoch_ratio": (energy["j_per_step_all_gpus"] / tp["energy"]["j_per_step_all_gpus"]
+                                                           if tp.get("energy") else None)}
         print(json.dumps(line), flush=True)
-    if world > 1:
-        # tear down our NCCL communicator at the same point on every rank, then torch's
-        barrier()
-        eng.close()
-        dist.barrier()
-        dist.destroy_process_group()
+    finish(D)
+    return 0
+
+
+def finish(D):
+    if D.world > 1:
+        D.barrier()
+        D.dist.destroy_process_group()
         sys.stdout.flush()
         sys.stderr.flush()
         os._exit(0)
+
+
+def stamped_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture
+    (profiles/traffic.json: {abi_call: {dram_bytes_per_launch, commit, ...}})."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        d = json.load(open(path)).get(kernel)
+        if d:
+            return {"dram_bytes_per_launch": d["dram_bytes_per_launch"],
+                    "source": f"ncu --set full, commit {d.get('commit')}, {d.get('shape', '')}".strip(", ")}
+    except Exception:
+        pass
+    return {"dram_bytes_per_launch": None, "source": "no committed ncu capture for this kernel"}
+
+
+def time_inference(eng, D, steps, use_graph, peak):
+    """Forward-only (config C5 at the engine's k): samples/s over graph replays, max over ranks."""
+    import torch
+    from paper_2508_00960_b200.engine import pp_forward_flops
+    eng.forward_only(0)
+    if use_graph:
+        eng.capture_inference()
+    for _ in range(3):
+        eng.forward_only(0, graph=use_graph)
+    S = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    D.barrier()
+    e0.record(S)
+    for _ in range(steps):
+        eng.forward_only(0, graph=use_graph)
+    e1.record(S)
+    D.barrier()
+    ms = D.reduce([e0.elapsed_time(e1) / steps])[0]
+    tf = eng.R * pp_forward_flops(eng.n, eng.p, eng.k, eng.L, eng.B) / (ms / 1e3) / 1e12
+    return {"config": f"C5: forward-only n={eng.n}, L={eng.L}, p={eng.p}, k={eng.k}, batch {eng.B}",
+            "value": eng.B / (ms / 1e3), "unit": "samples/s", "ms_per_batch": ms, "tflops_per_gpu": tf,
+            "frac_of_burst": tf / peak, "gpu_launches_per_batch": eng.infer_launch_count}
+
+
+def run_inference_sweep(args, cfg, D, uid, peak):
+    """--config c5: forward-only samples/s for k in 32..512 (BASELINE configs[4])."""
+    import torch
+    from paper_2508_00960_b200.engine import PhantomEngine
+    n, p, L, B = cfg["n"], cfg["p"], cfg["layers"], cfg["batch"]
+    rows = []
+    for k in C5_KS:
+        eng = PhantomEngine(n, p, k, L, B, world=D.world, rank=D.rank, device=D.local, uid=uid if k == C5_KS[0] else
+                            D.uid(), lr=3e-6, dtype=torch.bfloat16)
+        g = torch.Generator(device="cuda").manual_seed(5)
+        xs = [torch.randn((B, eng.s), generator=g, device="cuda").bfloat16() for _ in range(eng.R)]
+        eng.set_batch(xs, xs, 0)
+        r = time_inference(eng, D, args.steps, not args.no_graph, peak)
+        r["k"] = k
+        r["fused"] = bool(eng.fused)
+        rows.append(r)
+        D.barrier()
+        eng.close()
+        del eng
+        torch.cuda.empty_cache()
+    if D.rank == 0:
+        best = max(rows, key=lambda r: r["value"])
+        print(json.dumps({
+            "metric": "FFN forward-only inference samples/s (C5 k sweep)", "value": [r["value"] for r in rows],
+            "unit": "samples/s", "n_gpus": D.world, "steps": args.steps, "warmup": 3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"phantom FFN c5: n={n}, L={L}, p={p}, batch {B}, k in {list(C5_KS)}",
+                       "global_batch": B, "parallelism": f"phantom pp{p} over {D.world} GPU(s)"},
+            "sweep": rows, "roofline": {"bound": "tensor", "achieved": best["tflops_per_gpu"], "peak": peak,
+                                        "unit": "TFLOP/s", "frac": best["frac_of_burst"], "traffic": None}}), flush=True)
+    finish(D)
     return 0
+
+
+def time_e2e(eng, D, xs, ts, steps, use_graph, B):
+    import torch
+    xh = torch.stack([x.cpu() for x in xs]).pin_memory()
+    th = torch.stack([t_.cpu() for t_ in ts]).pin_memory()
+    h2d = 2 * xh.numel() * xh.element_size()
+    S = torch.cuda.current_stream()
+    D.barrier()
+    q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    q0.record(S)
+    ready = eng.load_batch_async(xh, th, eng.parity)
+    prev_done = None
+    for i in range(steps):
+        S.wait_event(ready)
+        par = eng.parity
+        eng.step(graph=use_graph)
+        done = torch.cuda.Event()
+        done.record(S)
+        if i + 1 < steps:
+            # the next batch goes into the other parity's buffers, last read by step i-1:
+            # its H2D overlaps step i
+            if prev_done is not None:
+                eng.copy_stream.wait_event(prev_done)
+            ready = eng.load_batch_async(xh, th, 1 - par)
+        prev_done = done
+        eng.read_loss()                              # D2H of the step's loss (+ non-finite flag)
+    q1.record(S)
+    D.barrier()
+    te = D.reduce([q0.elapsed_time(q1) / steps])[0]
+    return {"value": B / (te / 1e3), "unit": "samples/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8}
+
+
+def time_r1_shapes(cfg, D, xs, ts, args, peak, peak_sus):
+    """The same C3 step with one logical rank per launch (group=1): the per-GPU kernels of the
+    8-GPU run (per-rank forward, per-rank weight-gradient + recurrence LPT launches at s = n/p),
+    on this one GPU.  Exchanges stay in HBM, so this is the 8-GPU step's compute bound."""
+    import torch
+    from paper_2508_00960_b200.engine import PhantomEngine, pp_step_flops
+    n, p, k, L, B = cfg["n"], cfg["p"], cfg["k"], cfg["layers"], cfg["batch"]
+    eng = PhantomEngine(n, p, k, L, B, lr=3e-6, dtype=torch.bfloat16, group=1)
+    eng.set_batch(xs, ts, 0)
+    eng.set_batch(xs, ts, 1)
+    eng.step(graph=False)
+    eng.capture()
+    for _ in range(3):
+        eng.step()
+    ms = timed_steps(eng, D, args.steps)
+    seq = profile(eng, D)
+    kernels, kern_ms = kernel_table(seq, peak, steps=3)
+    flops = p * pp_step_flops(n, p, k, L, B)
+    eng.close()
+    return {"what": "C3 step with one logical rank per launch (the per-GPU launch shapes of C3 on 8 GPUs), 1 GPU",
+            "ms_per_step": ms, "samples_per_s": B / (ms / 1e3), "step_tflops": flops / (ms / 1e3) / 1e12,
+            "step_frac_of_sustained": flops / (ms / 1e3) / 1e12 / peak_sus,
+            "kernel_sum_ms_per_step": kern_ms,
+            "kernel_sum_frac_of_burst": flops / (kern_ms / 1e3) / 1e12 / peak,
+            "kernel_sum_frac_of_sustained": flops / (kern_ms / 1e3) / 1e12 / peak_sus,
+            "launches_per_step": eng.launch_count, "kernels": kernels}
+
+
+def run_tp(args, cfg, D, eng, uid):
+    """The same-width Megatron tensor-parallel FFN (TPEngine) on the same GPUs, same batch."""
+    import torch
+    from paper_2508_00960_b200 import _lib, kernels
+    from paper_2508_00960_b200.schedule import tp_comm_bytes_per_step
+    from paper_2508_00960_b200.tensor_parallel import TPEngine, tp_step_flops
+    n, L, B = cfg["n"], cfg["layers"], cfg["batch"]
+    world = D.world
+    ctx = eng.ctx if eng is not None else _lib.Context(1, 0, D.local)
+    # full replicated input / teacher targets of the dense-width task
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1234)
+    X = torch.randn((B, n), generator=g, device="cuda").to(torch.bfloat16)
+    Xr = torch.empty_like(X)
+    ctx.call("ppx_bias_act", _lib.PPX_BF16, B, n, X.data_ptr(), n, None, 0, Xr.data_ptr(), n,
+             torch.cuda.current_stream().cuda_stream)
+    gt = torch.Generator(device="cuda")
+    gt.manual_seed(99)
+    W = (torch.randn((n, n), generator=gt, device="cuda") / n ** 0.5).to(torch.bfloat16)
+    T = kernels.gemm(Xr, W, transpose_b=True, out_dtype=torch.bfloat16, relu=True, ctx=ctx)
+    del W, Xr
+    torch.cuda.synchronize()
+    if eng is not None:
+        D.barrier()
+        eng.close()                      # free the phantom engine's graphs + communicator first
+    else:
+        ctx.close()
+    torch.cuda.empty_cache()
+    tpe = TPEngine(n, L, B, world=world, rank=D.rank, device=D.local,
+                   uid=None if world == 1 else D.uid(), lr=3e-6, dtype=torch.bfloat16)
+    tpe.set_batch(X, T, 0)
+    tpe.set_batch(X, T, 1)
+    del X, T
+    tpe.step(graph=False)
+    tpe.read_loss()
+    tpe.capture()
+    for _ in range(2):
+        tpe.step()
+    tpe.read_loss()
+    steps = max(3, min(args.steps, 10))
+    ms = timed_steps(tpe, D, steps)
+    energy = energy_window(tpe, D, ms, args.energy_seconds)
+    loss = tpe.read_loss()
+    flops = tp_step_flops(n, world, L, B)
+    out = {"pipeline": f"Megatron tensor-parallel FFN n={n}, L={L}, batch {B}, column/row pairs, "
+                       f"{world} GPU(s), same kernels, SGD fused", "value": B / (ms / 1e3), "unit": "samples/s",
+           "ms_per_step": ms, "steps": steps, "step_tflops_per_gpu": flops / (ms / 1e3) / 1e12,
+           "energy": energy, "comm_bytes_per_step_per_gpu": tp_comm_bytes_per_step(n, L, B, world), "loss": loss,
+           "gpu_launches": tpe.launch_count * steps}
+    D.barrier()
+    tpe.close()
+    return out
 
 
 if __name__ == "__main__":

@@ -166,20 +166,13 @@ ppx_status ppx_forward_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_i
 ppx_status ppx_backward_delta_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B,
                                 ppx_act act_prev, void* stream);
 
-/* ---- NVLink peer memory: the phantom all-gather (collectives.py:115-120, 337-339) as direct
-   stores from the compression GEMM's epilogue into every peer's phantom buffer, with per-layer
-   flags instead of an NCCL kernel.  Regions come from ppx_peer_alloc (cudaMalloc + IPC handle,
-   zero-filled, freed by ppx_destroy); the 64-byte handles are exchanged by the caller (any
-   channel) and mapped with ppx_peer_open (closed by ppx_destroy). ----------------------------- */
+/* ---- NVLink peer memory (IPC regions every GPU maps): the fused forward's in-kernel phantom
+   all-gather (collectives.py:115-120, 337-339) and the NVLink reduce-scatter store straight into
+   them.  Regions come from ppx_peer_alloc (cudaMalloc + IPC handle, zero-filled, freed by
+   ppx_destroy); the 64-byte handles are exchanged by the caller (any channel) and mapped with
+   ppx_peer_open (closed by ppx_destroy). -------------------------------------------------------- */
 ppx_status ppx_peer_alloc(ppx_ctx* ctx, int64_t bytes, void** ptr, uint8_t handle[64]);
 ppx_status ppx_peer_open(ppx_ctx* ctx, const uint8_t handle[64], void** peer_ptr);
-/* ppx_compress_n whose epilogue also writes each phantom tile at the same offset of the n_peers
-   buffers peer_phantoms[r] (peer mappings of the other GPUs' phantom buffers). */
-ppx_status ppx_compress_push(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B,
-                             void* phantoms, int32_t n_peers, void* const* peer_phantoms, void* stream);
-/* *counter += 1, then every flags[i] (an int32 in a peer's region) = *counter (release, system
-   scope).  Stream-ordered after the pushes it publishes. */
-ppx_status ppx_peer_signal(ppx_ctx* ctx, int32_t n, int32_t* const* flags, int32_t* counter, void* stream);
 /* Fused compression + phantom all-gather + forward of one layer for the n local ranks, ONE
    launch of the 2-SM kernel (bf16): the compression tiles store their phantoms into `phantoms`
    and into every peer's copy (NVLink), then add 1 to every arrive[i] (own counter first); the
@@ -216,17 +209,6 @@ ppx_status ppx_error_phantoms_scatter(ppx_ctx* ctx, ppx_dtype dt, int32_t n, con
 ppx_status ppx_reduce_received(ppx_ctx* ctx, ppx_dtype dt, int32_t R, int64_t slot_elems, int32_t world,
                                int32_t rank, const void* stage, const void* own, void* out,
                                const int32_t* counter, int32_t* epoch, int32_t* bad, void* stream);
-/* The phantom all-gather as one NVLink kernel: copies `bytes` (multiple of 16) at src to dsts[i]
-   (peer mappings, same offsets) with 16-byte posted stores, then — once every CTA has fenced —
-   *counter += 1 and every flags[i] = *counter (release, system scope).  Pairs with ppx_peer_wait. */
-ppx_status ppx_peer_push(ppx_ctx* ctx, const void* src, int64_t bytes, int32_t n, void* const* dsts,
-                         int32_t* const* flags, int32_t* counter, void* stream);
-/* *counter += 1, then wait until every flags[i] (local int32s written by the peers) >= *counter
-   (acquire, system scope).  After PPX_PEER_TIMEOUT_S seconds (default 30) it sets bit 1 of *bad
-   and returns instead of hanging. */
-ppx_status ppx_peer_wait(ppx_ctx* ctx, int32_t n, int32_t* const* flags, int32_t* counter, int32_t* bad,
-                         void* stream);
-
 /* phantom.py:169-182 (+ training.py:66-69 scaling) — standalone output delta and loss partial.
    `pre` is the pre-activation (or the layer output: ReLU'(pre) == (y > 0)). */
 ppx_status ppx_output_delta(ppx_ctx* ctx, ppx_dtype dt, int32_t B, int32_t s, ppx_act act,
@@ -318,6 +300,14 @@ ppx_status ppx_colsum(ppx_ctx* ctx, ppx_dtype dt, int32_t rows, int32_t cols, co
 ppx_status ppx_optimizer_step(ppx_ctx* ctx, int32_t kind, const float* hyper, float* params,
                               const float* grad, float* adam_m, float* adam_v, int64_t n,
                               ppx_dtype dt, void* w_copy, int* bad, void* stream);
+
+/* training.py:92-105 (t incremented per step, training.py:297-300) — advances the device step
+   counter *step and writes the Adam bias corrections hyper[4] = 1 - beta1^t, hyper[5] = 1 - beta2^t
+   on `stream`.  hyper = [lr, beta1, beta2, eps, 1 - beta1^t, 1 - beta2^t] (fp32, device).  The
+   engine issues it first in every step, so graph replays and back-to-back steps need no host
+   write. */
+ppx_status ppx_hyper_advance(ppx_ctx* ctx, float* hyper, int32_t* step, double beta1, double beta2,
+                             void* stream);
 
 /* core.py:39-61 gemm: C[M,N] = op(a) . op(b), op(a) = a [M,K] or a^T (a stored [K,M]),
    op(b) = b [K,N] or b^T (b stored [N,K]).  out_dt selects C's element type. */

@@ -101,7 +101,6 @@ _SIGS = {
     "ppx_peek_error": (_i32, []),
     "ppx_peer_alloc": (_i32, [_vp, _i64, ctypes.POINTER(_vp), ctypes.c_char_p]),
     "ppx_peer_open": (_i32, [_vp, ctypes.c_char_p, ctypes.POINTER(_vp)]),
-    "ppx_compress_push": (_i32, [_vp, _i32, _i32, ctypes.POINTER(RankIO), _i32, _vp, _i32, ctypes.POINTER(_vp), _vp]),
     "ppx_forward_fused": (_i32, [_vp, _i32, _i32, ctypes.POINTER(RankIO), _i32, _i32, _vp, _i32, _f32, _f32, _fp,
                                    ctypes.POINTER(Exchange), _vp]),
     "ppx_error_phantoms_scatter": (_i32, [_vp, _i32, _i32, ctypes.POINTER(RankIO), _i32, _vp, ctypes.POINTER(Scatter),
@@ -109,9 +108,6 @@ _SIGS = {
     "ppx_reduce_received": (_i32, [_vp, _i32, _i32, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ppx_backward_fused": (_i32, [_vp, _i32, _i32, ctypes.POINTER(WgradItem), _i32, ctypes.POINTER(RankIO), _i32, _i32,
                                    _vp]),
-    "ppx_peer_push": (_i32, [_vp, _vp, _i64, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp]),
-    "ppx_peer_signal": (_i32, [_vp, _i32, ctypes.POINTER(_vp), _vp, _vp]),
-    "ppx_peer_wait": (_i32, [_vp, _i32, ctypes.POINTER(_vp), _vp, _vp, _vp]),
     "ppx_reduce_scatter": (_i32, [_vp, _i32, _vp, _i64, _i32, _vp]),
     "ppx_all_reduce_f32": (_i32, [_vp, _fp, _i64, _vp]),
     "ppx_all_reduce": (_i32, [_vp, _i32, _vp, _i64, _vp]),
@@ -122,6 +118,7 @@ _SIGS = {
                                   _vp, _i64, _vp, _i64, _fp, _vp]),
     "ppx_colsum": (_i32, [_vp, _i32, _i32, _i32, _vp, _i64, _fp, _i32, _vp]),
     "ppx_optimizer_step": (_i32, [_vp, _i32, _fp, _fp, _fp, _fp, _fp, _i64, _i32, _vp, _vp, _vp]),
+    "ppx_hyper_advance": (_i32, [_vp, _vp, _vp, ctypes.c_double, ctypes.c_double, _vp]),
     "ppx_gemm": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _i64, _i32, _vp, _i64,
                         _i32, ctypes.POINTER(Epilogue), _vp]),
     "ppx_gemm_update": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _i64, _i32,

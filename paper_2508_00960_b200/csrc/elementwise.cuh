@@ -165,6 +165,20 @@ inline cudaError_t launch_optimizer(bool adam, const float* hyper, float* w, con
   return cudaGetLastError();
 }
 
+// Adam step counter advanced on the device (training.py:95: t += 1 before the bias corrections):
+// hyper[4] = 1 - beta1^t, hyper[5] = 1 - beta2^t in double, so CUDA-graph replays never need a
+// host write and steps may be issued back to back.
+__global__ void hyper_advance_kernel(float* hyper, int* step, double beta1, double beta2) {
+  const int t = *step + 1;
+  *step = t;
+  hyper[4] = (float)(1.0 - pow(beta1, (double)t));
+  hyper[5] = (float)(1.0 - pow(beta2, (double)t));
+}
+inline cudaError_t launch_hyper_advance(float* hyper, int* step, double b1, double b2, cudaStream_t st) {
+  hyper_advance_kernel<<<1, 1, 0, st>>>(hyper, step, b1, b2);
+  return cudaGetLastError();
+}
+
 // ---- casts and activations ------------------------------------------------------------------
 __global__ void cast_kernel(bool src_f32, const void* src, bool dst_f32, void* dst, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -205,86 +219,6 @@ inline cudaError_t launch_relu_mask(bool f32, int rows, int cols, void* x, int64
 }
 
 
-// ---- NVLink peer signalling (phantom exchange without NCCL) ------------------------------------
-// Each GPU keeps per-(layer, source) int32 flags in IPC-shared memory and two local counters per
-// layer that advance once per use in lockstep on every GPU: the sender stores its new counter
-// value into every peer's flag after its phantom stores; the receiver waits until every source's
-// flag reached its own new counter value.  Graph-replay safe (no resets); a receiver that waits
-// longer than `timeout_ns` sets bit 1 of *bad and stops waiting (never hangs the GPU).
-constexpr int MAX_PEERS = 7;
-struct PeerFlags {
-  int* f[MAX_PEERS];
-};
-
-__global__ void peer_signal_kernel(int n, PeerFlags flags, int* counter) {
-  if (threadIdx.x != 0) return;
-  const int v = *counter + 1;
-  *counter = v;
-  __threadfence_system();
-  for (int i = 0; i < n; ++i) asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(flags.f[i]), "r"(v) : "memory");
-}
-
-__global__ void peer_wait_kernel(int n, PeerFlags flags, int* counter, int* bad, unsigned long long timeout_ns) {
-  __shared__ int target;
-  if (threadIdx.x == 0) {
-    target = *counter + 1;
-    *counter = target;
-  }
-  __syncthreads();
-  if ((int)threadIdx.x < n) {
-    unsigned long long t0, t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    int x;
-    for (;;) {
-      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(x) : "l"(flags.f[threadIdx.x]) : "memory");
-      if (x >= target) break;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > timeout_ns) {
-        if (bad) atomicOr(bad, 2);
-        break;
-      }
-      __nanosleep(64);
-    }
-  }
-  __syncthreads();
-  __threadfence_system();
-}
-
-// The phantom all-gather as ONE kernel over NVLink: every CTA copies a strided share of this
-// GPU's phantom chunk (16-byte vectors, read once from local HBM) into the same offset of every
-// peer's buffer (posted NVLink stores), then fences at system scope; the last CTA to finish
-// publishes the new counter value into every peer's flag (release) — peer_wait_kernel consumes it.
-struct PeerPtrs {
-  char* p[MAX_PEERS];
-};
-__global__ void peer_push_kernel(const uint4* __restrict__ src, long long n16, int n, PeerPtrs dst, PeerFlags flags,
-                                 int* counter, unsigned int* arrive) {
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) {
-    const uint4 v = src[i];
-#pragma unroll 1
-    for (int r = 0; r < n; ++r) reinterpret_cast<uint4*>(dst.p[r])[i] = v;
-  }
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int prev = atomicAdd(arrive, 1u);
-    if (prev == gridDim.x - 1) {
-      *arrive = 0u;
-      const int v = *counter + 1;
-      *counter = v;
-      __threadfence_system();
-      for (int r = 0; r < n; ++r)
-        asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(flags.f[r]), "r"(v) : "memory");
-    }
-  }
-}
-inline cudaError_t launch_peer_push(const void* src, long long bytes, int n, const PeerPtrs& dst, const PeerFlags& f,
-                                    int* counter, unsigned int* arrive, int blocks, cudaStream_t st) {
-  peer_push_kernel<<<blocks, 512, 0, st>>>(reinterpret_cast<const uint4*>(src), bytes / 16, n, dst, f, counter,
-                                           arrive);
-  return cudaGetLastError();
-}
 
 // Owner side of the NVLink reduce-scatter: wait until every source GPU's error-compression tiles
 // for this GPU's slots have arrived (wrap-safe counter >= (epoch+1) * per_epoch), then
@@ -358,16 +292,6 @@ inline cudaError_t launch_reduce_received(const ReduceArgs& a, cudaStream_t st) 
   if (blocks > 148) blocks = 148;   // all resident: every block reads the epoch before the last bumps it
   if (blocks < 1) blocks = 1;
   reduce_received_kernel<<<(int)blocks, 256, 0, st>>>(a);
-  return cudaGetLastError();
-}
-
-inline cudaError_t launch_peer_signal(int n, const PeerFlags& f, int* counter, cudaStream_t st) {
-  peer_signal_kernel<<<1, 32, 0, st>>>(n, f, counter);
-  return cudaGetLastError();
-}
-inline cudaError_t launch_peer_wait(int n, const PeerFlags& f, int* counter, int* bad, unsigned long long timeout_ns,
-                                    cudaStream_t st) {
-  peer_wait_kernel<<<1, 32, 0, st>>>(n, f, counter, bad, timeout_ns);
   return cudaGetLastError();
 }
 

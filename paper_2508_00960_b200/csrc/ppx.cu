@@ -35,7 +35,6 @@ struct ppx_ctx {
   std::vector<std::pair<char*, size_t>> ws;
   std::vector<void*> ipc_own;      // ppx_peer_alloc regions (cudaFree at destroy)
   std::vector<void*> ipc_mapped;   // ppx_peer_open mappings (cudaIpcCloseMemHandle at destroy)
-  unsigned int* push_arrive = nullptr;   // ppx_peer_push's CTA arrival counter (self-resetting)
   unsigned int* fuse_done = nullptr;     // fused launches' CTA exit counter (self-resetting)
   unsigned int* reduce_done = nullptr;   // ppx_reduce_received's block exit counter (self-resetting)
 };
@@ -820,7 +819,6 @@ ppx_status ppx_destroy(ppx_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (auto& c : ctx->ws) cudaFree(c.first);
   for (void* m : ctx->ipc_mapped) cudaIpcCloseMemHandle(m);
-  if (ctx->push_arrive) cudaFree(ctx->push_arrive);
   if (ctx->fuse_done) cudaFree(ctx->fuse_done);
   if (ctx->reduce_done) cudaFree(ctx->reduce_done);
   for (void* m : ctx->ipc_own) cudaFree(m);
@@ -1104,9 +1102,7 @@ ppx_status ppx_error_phantoms_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx
 // ---- NVLink peer memory: the phantom all-gather as NVLink stores from the compression GEMM ----
 ppx_status ppx_peer_alloc(ppx_ctx* ctx, int64_t bytes, void** ptr, uint8_t* handle) {
   if (!ctx || bytes <= 0 || !ptr || !handle) return PPX_E_CONFIG;
-  if (!ctx->push_arrive) {   // push / reduce exit counters (allocated here: never during capture)
-    CUDA_TRY(ctx, cudaMalloc(&ctx->push_arrive, sizeof(unsigned int)));
-    CUDA_TRY(ctx, cudaMemset(ctx->push_arrive, 0, sizeof(unsigned int)));
+  if (!ctx->reduce_done) {   // reduce exit counter (allocated here: never during capture)
     CUDA_TRY(ctx, cudaMalloc(&ctx->reduce_done, sizeof(unsigned int)));
     CUDA_TRY(ctx, cudaMemset(ctx->reduce_done, 0, sizeof(unsigned int)));
   }
@@ -1130,70 +1126,6 @@ ppx_status ppx_peer_open(ppx_ctx* ctx, const uint8_t* handle, void** peer_ptr) {
   CUDA_TRY(ctx, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
   ctx->ipc_mapped.push_back(p);
   *peer_ptr = p;
-  return PPX_OK;
-}
-
-ppx_status ppx_compress_push(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B,
-                             void* phantoms, int32_t n_peers, void* const* peer_phantoms, void* stream) {
-  if (!ctx) return PPX_E_CONFIG;
-  if (n < 1 || !io || n_peers < 0 || n_peers > ppx::MAX_REP || (n_peers && !peer_phantoms))
-    return fail(ctx, PPX_E_CONFIG, "ppx_compress_push: bad arguments");
-  Builder b(ctx, dt, stream);
-  for (int i = 0; i < n; ++i) {
-    ppx_status s = add_compress(ctx, dt, b, io[i], B, phantoms);
-    if (s != PPX_OK) return s;
-    Problem& pr = b.P.probs[b.P.nprobs - 1];
-    pr.epi.nrep = n_peers;
-    for (int r = 0; r < n_peers; ++r)
-      pr.epi.rep_off[r] = (long long)((const char*)peer_phantoms[r] - (const char*)phantoms);
-  }
-  return b.launch();
-}
-
-static ppx_status peer_flags(ppx_ctx* ctx, int32_t n, int32_t* const* flags, ppx::PeerFlags& f) {
-  if (n < 0 || n > ppx::MAX_PEERS || (n && !flags)) return fail(ctx, PPX_E_CONFIG, "peer flags: bad arguments");
-  memset(&f, 0, sizeof(f));
-  for (int i = 0; i < n; ++i) f.f[i] = flags[i];
-  return PPX_OK;
-}
-
-ppx_status ppx_peer_signal(ppx_ctx* ctx, int32_t n, int32_t* const* flags, int32_t* counter, void* stream) {
-  if (!ctx || !counter) return PPX_E_CONFIG;
-  ppx::PeerFlags f;
-  ppx_status s = peer_flags(ctx, n, flags, f);
-  if (s != PPX_OK) return s;
-  CUDA_TRY(ctx, ppx::launch_peer_signal(n, f, counter, (cudaStream_t)stream));
-  return PPX_OK;
-}
-
-ppx_status ppx_peer_push(ppx_ctx* ctx, const void* src, int64_t bytes, int32_t n, void* const* dsts,
-                         int32_t* const* flags, int32_t* counter, void* stream) {
-  if (!ctx || !src || !counter || bytes < 0 || bytes % 16 || n < 0 || n > ppx::MAX_PEERS || (n && !dsts))
-    return fail(ctx, PPX_E_CONFIG, "ppx_peer_push: bad arguments (bytes must be a multiple of 16)");
-  ppx::PeerFlags f;
-  ppx_status s = peer_flags(ctx, n, flags, f);
-  if (s != PPX_OK) return s;
-  ppx::PeerPtrs d;
-  memset(&d, 0, sizeof(d));
-  for (int i = 0; i < n; ++i) d.p[i] = (char*)dsts[i];
-  if (!ctx->push_arrive) return fail(ctx, PPX_E_SEQUENCING, "ppx_peer_push before ppx_peer_alloc");
-  const char* env = getenv("PPX_PUSH_BLOCKS");
-  int blocks = env ? atoi(env) : 64;
-  const long long need = (bytes / 16 + 511) / 512;
-  if (need < blocks) blocks = need > 0 ? (int)need : 1;
-  CUDA_TRY(ctx, ppx::launch_peer_push(src, bytes, n, d, f, counter, ctx->push_arrive, blocks, (cudaStream_t)stream));
-  return PPX_OK;
-}
-
-ppx_status ppx_peer_wait(ppx_ctx* ctx, int32_t n, int32_t* const* flags, int32_t* counter, int32_t* bad,
-                         void* stream) {
-  if (!ctx || !counter) return PPX_E_CONFIG;
-  ppx::PeerFlags f;
-  ppx_status s = peer_flags(ctx, n, flags, f);
-  if (s != PPX_OK) return s;
-  const char* env = getenv("PPX_PEER_TIMEOUT_S");
-  const double secs = env ? atof(env) : 30.0;
-  CUDA_TRY(ctx, ppx::launch_peer_wait(n, f, counter, bad, (unsigned long long)(secs * 1e9), (cudaStream_t)stream));
   return PPX_OK;
 }
 
@@ -1559,6 +1491,13 @@ ppx_status ppx_optimizer_step(ppx_ctx* ctx, int32_t kind, const float* hyper, fl
   cudaError_t e = ppx::launch_optimizer(kind == PPX_UPDATE_ADAM, hyper, params, grad, adam_m, adam_v, n,
                                         dt == PPX_FP32, w_copy, bad, (cudaStream_t)stream);
   return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "optimizer: %s", cudaGetErrorString(e));
+}
+
+ppx_status ppx_hyper_advance(ppx_ctx* ctx, float* hyper, int32_t* step, double beta1, double beta2, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (!hyper || !step) return fail(ctx, PPX_E_CONFIG, "ppx_hyper_advance: bad arguments");
+  cudaError_t e = ppx::launch_hyper_advance(hyper, step, beta1, beta2, (cudaStream_t)stream);
+  return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "hyper_advance: %s", cudaGetErrorString(e));
 }
 
 ppx_status ppx_gemm(ppx_ctx* ctx, ppx_dtype dt, int32_t M, int32_t N, int32_t K, const void* a, int64_t lda,

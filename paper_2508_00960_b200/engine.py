@@ -53,7 +53,24 @@ class PhantomEngine:
     def __init__(self, n: int, p: int, k: int, layers: int, batch: int, *, world: int = 1, rank: int = 0,
                  device: int = 0, uid: bytes | None = None, activation=Activation.RELU, reduction: str = "mean",
                  optimizer: str = "sgd", lr: float = 1e-4, betas=(0.9, 0.999), eps: float = 1e-8,
-                 dtype: torch.dtype = torch.bfloat16, seed: int = 0, ctx: _lib.Context | None = None):
+                 dtype: torch.dtype = torch.bfloat16, seed: int = 0, ctx: _lib.Context | None = None,
+                 fused: bool | None = None, nvrs: bool | None = None, group: int | None = None,
+                 bwd_fused: bool | None = None, store_output: bool = False, capture: bool = False):
+        """Launch-plan switches (None = the default plan; every plan computes the same step):
+
+        fused      compression + phantom all-gather + forward of a layer as ONE launch (bf16, s and k
+                   multiples of 64, <= 8 logical ranks per GPU); otherwise compression, NCCL
+                   all-gather on the comm stream, then the K-concatenated forward GEMM.
+        nvrs       (world > 1, bf16, k % 8 == 0) reduce-scatter through NVLink peer memory from the
+                   error-compression epilogue instead of NCCL; default when a GPU owns >= 2 ranks.
+        group      logical ranks per grouped launch (default all R; 1 = the per-GPU launch shapes of
+                   a run with one logical rank per GPU, on one GPU).
+        bwd_fused  weight gradients + error recurrence of a layer as one LPT-scheduled launch per
+                   group; default when each launch holds one logical rank.
+        store_output  keep the output layer's y (training steps never read it back).
+        capture    keep the raw weight gradients (fp32, flat layout) and every layer's delta of the
+                   last eager step (parity tests; CUDA-graph replays do not refresh the deltas).
+        """
         if n % p:
             raise ConfigurationError(f"n={n} not divisible by p={p}")
         if p % world:
@@ -79,6 +96,8 @@ class PhantomEngine:
         T, R, L, B = self.off["total"], self.R, layers, batch
         ldk = self.off["ldk"]
         f32 = torch.float32
+        if world > 1 and not self._dist_ready():
+            raise ConfigurationError("world > 1 needs torch.distributed initialised (IPC handles and barriers)")
         # parameters
         self.master = torch.zeros((R, L, T), dtype=f32, device=self.dev)
         # two compute copies (read w[par], the fused update writes w[1-par]); separate from the
@@ -91,6 +110,9 @@ class PhantomEngine:
             self.adam_v = torch.zeros_like(self.master)
             self.adam_bm = torch.zeros_like(self.bias)
             self.adam_bv = torch.zeros_like(self.bias)
+        self.capture_grads = capture
+        self.grad = torch.zeros_like(self.master) if capture else None
+        self.deltas = [None] * L            # capture: deltas[l][jj] = delta_l of the last eager step
         self.t = 0
         self._init_weights(seed)
         # activations: Y[parity][jj][l], l = 0 (input) .. L (output); targets per parity
@@ -102,62 +124,68 @@ class PhantomEngine:
                 self.Y[1][jj][l] = self.Y[0][jj][l]
         self.Tgt = [[torch.empty((B, s), dtype=dtype, device=self.dev) for _ in range(R)] for _ in range(2)]
         self.D = [[torch.empty((B, s), dtype=dtype, device=self.dev) for _ in range(2)] for _ in range(R)]
-        # phantom all-gather buffers; on multi-GPU runs the batch is split in two halves
-        # [2][p][B/2, ldk] so each half's all-gather hides behind the other half's GEMMs
-        self.halves = 2 if (world > 1 and B % 128 == 0 and os.environ.get("PPX_HALVES", "1") == "2") else 1
-        # NVLink phantom exchange (world > 1): the G buffers live in IPC-shared memory; the
-        # compression GEMM stores every phantom tile into all peers' G buffers and a per-layer
-        # flag replaces the NCCL all-gather (PPX_P2P=1; default NCCL)
         self.bad = torch.zeros(1, dtype=torch.int32, device=self.dev)
-        # default (PPX_FUSED=0 disables; bf16, 64-aligned s and k): compression + all-gather + forward of a layer as ONE launch of the
-        # 2-SM kernel — compression tiles store their phantoms into every GPU's buffer over
-        # NVLink and bump per-layer arrival counters, forward tiles wait in-kernel after their
-        # local-block segment
-        self.fused = (os.environ.get("PPX_FUSED", "1") != "0" and dtype == torch.bfloat16 and s % 64 == 0
-                      and k % 64 == 0 and p // world <= 8 and not os.environ.get("PPX_NOGROUP")
-                      and (world == 1 or self._dist_ready()))
-        self.p2p = int(os.environ.get("PPX_P2P", "0")) if world > 1 and self._dist_ready() else 0
-        if self.fused and world > 1 and not self.p2p:
-            self.p2p = 2
+        self.group = R if group is None else max(1, min(int(group), R))
+        auto_fused = (dtype == torch.bfloat16 and s % 64 == 0 and k % 64 == 0 and R <= 8 and self.group == R)
+        if fused and not auto_fused:
+            raise ConfigurationError("fused forward needs bf16, s and k multiples of 64, <= 8 ranks per GPU and "
+                                     "one group per layer")
+        self.fused = auto_fused if fused is None else bool(fused)
+        # NVLink reduce-scatter (world > 1, bf16): default when a GPU owns >= 2 logical ranks (C3 on
+        # 4 GPUs: 5.41 -> 5.31 ms); with one rank per GPU the NCCL reduce-scatter on the comm stream
+        # under the weight gradients is faster (C2 on 4 GPUs: 2.53 -> 2.70 ms)
+        nvrs_ok = world > 1 and dtype == torch.bfloat16 and R <= 8 and k % 8 == 0
+        if nvrs and not nvrs_ok:
+            raise ConfigurationError("NVLink reduce-scatter needs world > 1, bf16, <= 8 ranks per GPU and k % 8 == 0")
+        self.nvrs = (nvrs_ok and R >= 2) if nvrs is None else bool(nvrs)
+        # IPC-shared phantom / staging region (world > 1): needed by the fused forward's in-kernel
+        # all-gather and by the NVLink reduce-scatter
+        self.p2p = world > 1 and (self.fused or self.nvrs)
         if self.p2p:
-            self.halves = 1
             self._setup_p2p(dtype)
         else:
             self.G = [torch.zeros((p, B, ldk), dtype=dtype, device=self.dev) for _ in range(L)]
         if self.fused:
-            self.halves = 1
             self._setup_fused()
         self.H = [torch.zeros((p, B, ldk), dtype=dtype, device=self.dev) for _ in range(L)]
         # out-of-place reduce-scatter target (world > 1): this GPU's R received slots
         self.Hr = [torch.zeros((R, B, ldk), dtype=dtype, device=self.dev) for _ in range(L)] if world > 1 else None
         self.loss = torch.zeros(1, dtype=f32, device=self.dev)
-        self.hyper = torch.zeros(6, dtype=f32, device=self.dev)
-        self.hyper_host = torch.zeros(6, dtype=f32).pin_memory()
+        self.fence = torch.zeros(1, dtype=f32, device=self.dev)
+        # optimizer scalars [lr, beta1, beta2, eps, 1 - beta1^t, 1 - beta2^t]: the bias corrections
+        # are advanced on the device by the first launch of every step (graph replays need no host
+        # write, and no pinned buffer is rewritten while an earlier copy of it may be in flight)
+        b1, b2 = betas
+        self.hyper = torch.tensor([lr, b1, b2, eps, 0.0, 0.0], dtype=f32, device=self.dev)
+        self.tdev = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.out_host = torch.zeros(1, dtype=f32).pin_memory()
         self.bad_host = torch.zeros(1, dtype=torch.int32).pin_memory()
         if dtype == torch.float32:   # 3xTF32 hi/lo splits: reserve so graph capture never allocates
             per_call = 4 * B * s + 2 * p * B * ldk + 2 * T + 4 * s * ldk
             self.ctx.call("ppx_reserve_workspace", int(2 * 4 * per_call * 1.25) + (1 << 20))
-        self.comm_sms = int(os.environ.get("PPX_COMM_SMS", "0"))
-        # PPX_NOGROUP=1 launches every logical rank separately (emulates the R=1 launch shapes of an
-        # 8-GPU run on one GPU, for profiling)
-        self.group = 1 if os.environ.get("PPX_NOGROUP") else R
         self.graphs = [None, None]
+        self.infer_graphs = [None, None]
+        self.infer_launch_count = 0
         self.parity = 0
-        # training steps skip the output layer's y store (PPX_STORE_OUTPUT=1 keeps it)
-        self.skip_output = not os.environ.get("PPX_STORE_OUTPUT")
+        self.skip_output = not store_output
         # weight gradients + error recurrence of a layer as one LPT-scheduled launch (after the
-        # reduce-scatter): default with one logical rank per GPU, where either launch alone leaves
-        # ~1.4 rounds of tiles (PPX_BWD_FUSED=1/0 forces it on / off)
-        bf = os.environ.get("PPX_BWD_FUSED", "")
-        self.bwd_fused = dtype == torch.bfloat16 and (bf == "1" or (bf == "" and self.R == 1 and world > 1))
-        # timing experiments ONLY (wrong results): drop the backward reduce-scatter
-        self._dbg_skip_rs = bool(os.environ.get("PPX_DEBUG_SKIP_RS"))
-        self._dbg_skip_ag = bool(os.environ.get("PPX_DEBUG_SKIP_AG"))
+        # reduce-scatter): default when a launch holds one logical rank, where either launch alone
+        # leaves ~1.4 rounds of tiles
+        # (<= 16 problems per launch: 4 per logical rank)
+        auto_bf = dtype == torch.bfloat16 and self.group == 1 and (world > 1 or R > 1)
+        if bwd_fused and (dtype != torch.bfloat16 or self.group > 3):
+            raise ConfigurationError("fused backward needs bf16 and <= 3 logical ranks per launch group")
+        self.bwd_fused = auto_bf if bwd_fused is None else bool(bwd_fused)
         self._keep = []   # ctypes structs of the launch being built
         self._launches = 0
         self.launch_count = 0
         self.trace = []   # kernel-launching ABI calls of the last step body (profiling labels)
+        self._timing = None   # per-launch CUDA events (profile_step)
+        # algorithmic GEMM FLOPs per logical rank of each contraction
+        self._f_compress = 2 * B * s * k
+        self._f_forward = 2 * B * s * (s + (p - 1) * k)
+        self._f_error = 2 * B * s * (p - 1) * k
+        self._f_recurrence = 2 * B * s * (s + k)
 
     # ------------------------------------------------------------------------------------------
     @staticmethod
@@ -166,18 +194,18 @@ class PhantomEngine:
         return dist.is_available() and dist.is_initialized()
 
     def _setup_p2p(self, dtype):
-        """IPC region [L][p, B, ldk] phantoms + [L][world] int32 flags on every GPU, mapped by all
-        peers (handles exchanged over torch.distributed); identical layouts, so a peer address
-        is peer_base + (local address - local base)."""
+        """IPC region on every GPU, mapped by all peers (handles exchanged over torch.distributed):
+        [L][p, B, ldk] phantoms | [L] fused-forward arrival counters | [L] reduce-scatter arrival
+        counters | [L][world, R, B, ldk] reduce-scatter staging.  Identical layouts, so a peer
+        address is peer_base + (local address - local base)."""
         import torch.distributed as dist
         p, B, L, ldk, world = self.p, self.B, self.L, self.off["ldk"], self.world
         esz = torch.tensor([], dtype=dtype).element_size()
         gbytes = p * B * ldk * esz
         self._goff = [l * gbytes for l in range(L)]
-        self._foff = L * gbytes
-        self._coff = self._foff + ((L * world * 4 + 255) // 256) * 256    # per-layer arrival counters
+        self._coff = L * gbytes                                           # per-layer arrival counters
         self._rcoff = self._coff + ((L * 4 + 255) // 256) * 256           # reduce-scatter arrival counters
-        sbytes = world * self.R * B * ldk * esz                           # reduce-scatter staging per layer
+        sbytes = world * self.R * B * ldk * esz if self.nvrs else 0       # reduce-scatter staging per layer
         self._soff = [self._rcoff + ((L * 4 + 255) // 256) * 256 + l * sbytes for l in range(L)]
         nbytes = self._soff[0] + L * sbytes
         ptr = ctypes.c_void_p()
@@ -200,22 +228,6 @@ class PhantomEngine:
                                                  "version": 3}
         raw = torch.as_tensor(_Raw(self._pbase, nbytes), device=self.dev)
         self.G = [raw[o:o + gbytes].view(dtype).view(p, B, ldk) for o in self._goff]
-        self._sigcnt = torch.zeros(L, dtype=torch.int32, device=self.dev)
-        self._waitcnt = torch.zeros(L, dtype=torch.int32, device=self.dev)
-        n = len(self._peers)
-        mk = lambda addrs: (ctypes.c_void_p * max(n, 1))(*addrs)   # noqa: E731
-        self._push_dst = [mk([self._peer_base[g] + o for g in self._peers]) for o in self._goff]
-        # flag (l, src) lives at foff + 4 (l * world + src) in the region of the GPU that waits
-        self._sig_dst = [mk([self._peer_base[g] + self._foff + 4 * (l * world + self.rank) for g in self._peers])
-                         for l in range(L)]
-        self._wait_src = [mk([self._pbase + self._foff + 4 * (l * world + g) for g in self._peers])
-                          for l in range(L)]
-        # NVLink reduce-scatter (bf16, with the IPC region): default when a GPU owns >= 2 logical
-        # ranks (C3 on 4 GPUs: 5.41 -> 5.31 ms); with one rank per GPU the per-slot error
-        # compression tiles worse than the NCCL path (C2 on 4 GPUs: 2.53 -> 2.70 ms), so it is
-        # opt-in there (PPX_NVRS=1; PPX_NVRS=0 always NCCL)
-        nv = os.environ.get("PPX_NVRS", "")
-        self.nvrs = dtype == torch.bfloat16 and self.R <= 8 and (nv == "1" or (nv == "" and self.R >= 2))
         if self.nvrs:
             vpp = ctypes.POINTER(ctypes.c_void_p)
             base = lambda g: self._pbase if g == self.rank else self._peer_base[g]   # noqa: E731
@@ -307,6 +319,16 @@ class PhantomEngine:
         return {"local": m[0:s * lds].view(s, lds)[:, :s], "compressor": m[off["comp"]:off["comp"] + k * lds]
                 .view(k, lds)[:, :s], "decompressors": decs, "bias": self.bias[jj, l] if bias is None else bias}
 
+    def phantoms_view(self, l):
+        """[p, B, k] view of layer l's gathered phantoms (slot i = logical rank i's g_i)."""
+        return self.G[l][:, :, :self.k]
+
+    def received_view(self, l, jj):
+        """[B, k] view of the error phantoms r_j local rank jj received for layer l."""
+        if self.Hr is not None:
+            return self.Hr[l][jj, :, :self.k]
+        return self.H[l][self.local[jj], :, :self.k]
+
     def save_checkpoint(self, path, seed: int = 0, *, optimizer_state: bool = False):
         """PSHARD01 checkpoint of the weights (+ optimizer sidecar): every process writes its own
         logical ranks in place (checkpoint.py)."""
@@ -334,7 +356,7 @@ class PhantomEngine:
                         self.w[1 - par][jj, l].data_ptr(),
                         self.adam_m[jj, l].data_ptr() if kind == _lib.PPX_UPDATE_ADAM else None,
                         self.adam_v[jj, l].data_ptr() if kind == _lib.PPX_UPDATE_ADAM else None,
-                        None, self.bad.data_ptr())
+                        self.grad[jj, l].data_ptr() if self.capture_grads else None, self.bad.data_ptr())
         self._keep.append(u)
         return u
 
@@ -345,14 +367,23 @@ class PhantomEngine:
         return self.H[l].data_ptr() + j * self.B * self.off["ldk"] * self.H[l].element_size()
 
     _KERNEL_CALLS = {"ppx_compress", "ppx_forward_update", "ppx_forward_output", "ppx_error_phantoms", "ppx_wgrad",
-                     "ppx_backward_delta", "ppx_optimizer_step", "ppx_compress_n", "ppx_forward_n", "ppx_error_phantoms_n", "ppx_compress_push",
-                     "ppx_peer_signal", "ppx_peer_wait", "ppx_peer_push", "ppx_forward_fused",
-                     "ppx_error_phantoms_scatter", "ppx_reduce_received", "ppx_backward_fused",
-                     "ppx_backward_delta_n"}
+                     "ppx_backward_delta", "ppx_optimizer_step", "ppx_compress_n", "ppx_forward_n",
+                     "ppx_error_phantoms_n", "ppx_forward_fused", "ppx_error_phantoms_scatter", "ppx_reduce_received",
+                     "ppx_backward_fused", "ppx_backward_delta_n", "ppx_hyper_advance"}
 
-    def _call(self, name, *args):
-        """ctx.call that counts the launches of our own kernels (NCCL / memsets excluded)."""
+    def _call(self, name, *args, flops=0):
+        """ctx.call that counts the launches of our own kernels (NCCL / memsets excluded); under
+        profile_step() every kernel launch is bracketed by CUDA events on its stream and tagged
+        with its algorithmic GEMM FLOPs."""
+        timed = self._timing is not None and name in self._KERNEL_CALLS
+        if timed:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record()
         self.ctx.call(name, *args)
+        if timed:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            self._timing.append((name, e0, e1, flops))
         if name in self._KERNEL_CALLS:
             self._launches += 1
             self.trace.append(name)
@@ -375,121 +406,103 @@ class PhantomEngine:
         self._keep.append(arr)
         return arr
 
-    def _gh(self, l, h):
-        """Phantom buffer of batch half h of layer l ([p, B/H, ldk] at offset h)."""
-        Bh = self.B // self.halves
-        return self.G[l].data_ptr() + h * self.p * Bh * self.off["ldk"] * self.G[l].element_size()
+    def _chunks(self):
+        """Local-rank index ranges of the grouped launches."""
+        return [(c, min(c + self.group, self.R)) for c in range(0, self.R, self.group)]
 
     def _forward(self, par, S, train=True):
-        st, pdt, B, s, R, H = S.cuda_stream, self.pdt, self.B, self.s, self.R, self.halves
-        Bh = B // H
-        esz = self.Y[par][0][0].element_size()
-        rows = lambda t, h: t.data_ptr() + h * Bh * s * esz   # noqa: E731  (row block h of a [B, s] buffer)
+        st, pdt, B, s, R = S.cuda_stream, self.pdt, self.B, self.s, self.R
         mean = self.reduction == "mean"
-        ag_done = {}
 
-        def compress(l, h):
-            ios = [self._io(jj, l, par, x=rows(self.Y[par][jj][l], h), ld_x=s) for jj in range(R)]
-            if self.p2p == 2:   # compress, then ONE NVLink push kernel (copy to peers + flag)
-                n = len(self._peers)
-                for c in range(0, R, self.group):
-                    self._call("ppx_compress_n", pdt, min(self.group, R - c), self._ios(ios[c:c + self.group]), Bh,
-                               self._gh(l, h), st)
-                own = self._gh(l, h) + self.rank * R * Bh * self.off["ldk"] * esz
-                nbytes = R * Bh * self.off["ldk"] * esz
-                off = own - self._pbase
-                dst = (ctypes.c_void_p * max(n, 1))(*[self._peer_base[g] + off for g in self._peers])
-                self._keep.append(dst)
-                self._call("ppx_peer_push", own, nbytes, n, dst, self._sig_dst[l], self._sigcnt[l:].data_ptr(), st)
-                return
-            if self.p2p:   # fused all-gather: NVLink stores from the epilogue, then the layer flag
-                n = len(self._peers)
-                for c in range(0, R, self.group):
-                    self._call("ppx_compress_push", pdt, min(self.group, R - c), self._ios(ios[c:c + self.group]),
-                               Bh, self._gh(l, h), n, self._push_dst[l], st)
-                self._call("ppx_peer_signal", n, self._sig_dst[l], self._sigcnt[l:].data_ptr(), st)
-                return
-            for c in range(0, R, self.group):
-                self._call("ppx_compress_n", pdt, min(self.group, R - c), self._ios(ios[c:c + self.group]), Bh,
-                           self._gh(l, h), st)
-            if self.world > 1 and not self._dbg_skip_ag:
-                self._join(S, self.comm_stream)
-                self._call("ppx_all_gather", pdt, self._gh(l, h), Bh * self.off["ldk"], R,
-                           self.comm_stream.cuda_stream)
-                ev = torch.cuda.Event()
-                ev.record(self.comm_stream)
-                ag_done[(l, h)] = ev
+        def ios_for(l, last):
+            ios = []
+            for jj in range(R):
+                kw = dict(x=self.Y[par][jj][l].data_ptr(), ld_x=s, out=self.Y[par][jj][l + 1].data_ptr(), ld_out=s)
+                if last:   # the output y itself is never read by the backward pass: not stored
+                    kw.update(out=None if self.skip_output else kw["out"], aux=self.D[jj][0].data_ptr(), ld_aux=s,
+                              target=self.Tgt[par][jj].data_ptr(), ld_t=s, colsum=self.gbias[jj, l].data_ptr())
+                ios.append(self._io(jj, l, par, **kw))
+            return ios
 
+        scales = lambda last: (1.0 / B if mean else 1.0, 0.5 / B if mean else 0.5,   # noqa: E731
+                               self.loss.data_ptr() if last else None)
         if self.fused:
             for l in range(self.L):
                 last = train and l == self.L - 1
-                ios = []
-                for jj in range(R):
-                    kw = dict(x=self.Y[par][jj][l].data_ptr(), ld_x=s, out=self.Y[par][jj][l + 1].data_ptr(), ld_out=s)
-                    if last:
-                        kw.update(out=None if self.skip_output else kw["out"], aux=self.D[jj][0].data_ptr(), ld_aux=s,
-                                  target=self.Tgt[par][jj].data_ptr(), ld_t=s, colsum=self.gbias[jj, l].data_ptr())
-                    ios.append(self._io(jj, l, par, **kw))
-                self._call("ppx_forward_fused", pdt, R, self._ios(ios), B, self.act.code, self.G[l].data_ptr(),
-                           int(last), 1.0 / B if mean else 1.0, 0.5 / B if mean else 0.5,
-                           self.loss.data_ptr() if last else None, ctypes.byref(self._ex[l][0]), st)
+                self._call("ppx_forward_fused", pdt, R, self._ios(ios_for(l, last)), B, self.act.code,
+                           self.G[l].data_ptr(), int(last), *scales(last), ctypes.byref(self._ex[l][0]), st,
+                           flops=R * (self._f_compress + self._f_forward))
+            if not train and self.world > 1:
+                # inference ends without the loss all-reduce that orders training steps across
+                # GPUs: fence here so the next call's phantom stores never reach a peer that is
+                # still reading this call's phantoms
+                self._call("ppx_all_reduce_f32", self.fence.data_ptr(), 1, st)
             return
-        # software pipeline over batch halves: the all-gather of one half overlaps the other
-        # half's GEMMs (H = 2 on multi-GPU runs; H = 1 has nothing to hide)
-        for h in range(H):
-            compress(0, h)
         for l in range(self.L):
             last = train and l == self.L - 1
-            for h in range(H):
-                if (l, h) in ag_done:
-                    S.wait_event(ag_done[(l, h)])
-                if self.p2p:
-                    self._call("ppx_peer_wait", len(self._peers), self._wait_src[l], self._waitcnt[l:].data_ptr(),
-                               self.bad.data_ptr(), st)
-                ios = []
-                for jj in range(R):
-                    kw = dict(x=rows(self.Y[par][jj][l], h), ld_x=s, out=rows(self.Y[par][jj][l + 1], h), ld_out=s)
-                    if last:   # the output y itself is never read by the backward pass: not stored
-                        kw.update(out=None if self.skip_output else kw["out"], aux=rows(self.D[jj][0], h), ld_aux=s,
-                                  target=rows(self.Tgt[par][jj], h), ld_t=s, colsum=self.gbias[jj, l].data_ptr())
-                    ios.append(self._io(jj, l, par, **kw))
-                for c in range(0, R, self.group):
-                    self._call("ppx_forward_n", pdt, min(self.group, R - c), self._ios(ios[c:c + self.group]), Bh,
-                               self.act.code, self._gh(l, h), int(last), 1.0 / B if mean else 1.0,
-                               0.5 / B if mean else 0.5, self.loss.data_ptr() if last else None, st)
-                if l + 1 < self.L:
-                    compress(l + 1, h)
+            ios = [self._io(jj, l, par, x=self.Y[par][jj][l].data_ptr(), ld_x=s) for jj in range(R)]
+            for c0, c1 in self._chunks():
+                self._call("ppx_compress_n", pdt, c1 - c0, self._ios(ios[c0:c1]), B, self.G[l].data_ptr(), st,
+                           flops=(c1 - c0) * self._f_compress)
+            if self.world > 1:   # NCCL in-place all-gather of the contiguous phantom slots
+                self._join(S, self.comm_stream)
+                self._call("ppx_all_gather", pdt, self.G[l].data_ptr(), B * self.off["ldk"], R,
+                           self.comm_stream.cuda_stream)
+                self._join(self.comm_stream, S)
+            ios = ios_for(l, last)
+            for c0, c1 in self._chunks():
+                self._call("ppx_forward_n", pdt, c1 - c0, self._ios(ios[c0:c1]), B, self.act.code,
+                           self.G[l].data_ptr(), int(last), *scales(last), st, flops=(c1 - c0) * self._f_forward)
+
+    def _f_item(self, it):
+        """FLOPs of one weight-gradient request (d local 2Bs^2, d decompressors 2Bs(p-1)k,
+        d compressor 2Bsk)."""
+        B, s, k, p = self.B, self.s, self.k, self.p
+        f = 2 * B * s * s if it.parts & _lib.GRAD_LOCAL else 0
+        if p > 1:
+            f += 2 * B * s * (p - 1) * k if it.parts & _lib.GRAD_DEC else 0
+            f += 2 * B * s * k if it.parts & _lib.GRAD_COMP else 0
+        return f
 
     def _launch_wgrad(self, items, st):
         arr = (_lib.WgradItem * len(items))(*items)
         self._keep.append(arr)
-        self._call("ppx_wgrad", self.pdt, len(items), arr, st)
+        self._call("ppx_wgrad", self.pdt, len(items), arr, st, flops=sum(self._f_item(it) for it in items))
+
+    def _recurrence_io(self, jj, l, par, cur):
+        """[delta | r].[L ; C] -> delta_{l-1} with the ReLU'-mask and d-bias epilogue."""
+        return self._io(jj, l, par, x=self.D[jj][cur].data_ptr(), ld_x=self.s, out=self.D[jj][1 - cur].data_ptr(),
+                        ld_out=self.s, mask=self.Y[par][jj][l].data_ptr() if self.act is Activation.RELU else None,
+                        ld_m=self.s, received=self._received(l, self.local[jj]),
+                        colsum=self.gbias[jj, l - 1].data_ptr())
 
     def _backward(self, par, S):
         st, pdt, B, s, R, L = S.cuda_stream, self.pdt, self.B, self.s, self.R, self.L
         slot = B * self.off["ldk"]
         esz = self.H[0].element_size()
+        nvrs = self.nvrs
         cur = 0
         for l in range(L - 1, -1, -1):
-            if getattr(self, "nvrs", False) and self.p2p:
+            if self.capture_grads:
+                self.deltas[l] = [self.D[jj][cur].clone() for jj in range(R)]
+            ios = [self._io(jj, l, par, x=self.D[jj][cur].data_ptr(), ld_x=s) for jj in range(R)]
+            if nvrs:
                 # NVLink reduce-scatter: the error-compression epilogue copies every peer-owned
                 # slot into its owner's staging area; reduced after the weight gradients
-                ios = [self._io(jj, l, par, x=self.D[jj][cur].data_ptr(), ld_x=s) for jj in range(R)]
                 self._call("ppx_error_phantoms_scatter", pdt, R, self._ios(ios), B, self.H[l].data_ptr(),
-                           ctypes.byref(self._sc[l][0]), st)
-            elif self.group >= R and not os.environ.get("PPX_K3_PERRANK"):
+                           ctypes.byref(self._sc[l][0]), st, flops=R * self._f_error)
+            elif self.group >= R:
                 # one launch: slot i = sum_{local j != i} delta_j . D_{i->j}, every slot with a
                 # contributor overwritten (with R = 1 the own slot has none and stays zero: the
                 # reduce-scatter is out of place)
-                ios = [self._io(jj, l, par, x=self.D[jj][cur].data_ptr(), ld_x=s) for jj in range(R)]
-                self._call("ppx_error_phantoms_n", pdt, R, self._ios(ios), B, self.H[l].data_ptr(), st)
-            else:   # PPX_NOGROUP profiling: per-rank launches accumulating into zeroed slots
+                self._call("ppx_error_phantoms_n", pdt, R, self._ios(ios), B, self.H[l].data_ptr(), st,
+                           flops=R * self._f_error)
+            else:   # per-group launches accumulate into zeroed slots
                 self._call("ppx_zero", self.H[l].data_ptr(), self.H[l].numel() * esz, st)
                 for jj in range(R):
                     self._call("ppx_error_phantoms", pdt, ctypes.byref(self._layer(jj, l, par)), B,
-                               self.D[jj][cur].data_ptr(), s, self.H[l].data_ptr(), 1, st)
-            nvrs = getattr(self, "nvrs", False) and self.p2p
-            if self.world > 1 and not self._dbg_skip_rs and not nvrs:
+                               self.D[jj][cur].data_ptr(), s, self.H[l].data_ptr(), 1, st, flops=self._f_error)
+            if self.world > 1 and not nvrs:
                 self._join(S, self.comm_stream)
                 self._call("ppx_reduce_scatter_to", pdt, self.H[l].data_ptr(), self.Hr[l].data_ptr(), slot, R,
                            self.comm_stream.cuda_stream)
@@ -499,16 +512,15 @@ class PhantomEngine:
                 j = self.local[jj]
                 items = [_lib.WgradItem(ctypes.pointer(self._layer(jj, l, par)), _lib.GRAD_LOCAL | _lib.GRAD_DEC, B,
                                         self.D[jj][cur].data_ptr(), s, self.Y[par][jj][l].data_ptr(), s,
-                                        self.G[l].data_ptr(), None, None, ctypes.pointer(self._update(jj, l, par)),
-                                        self.halves)]
+                                        self.G[l].data_ptr(), None, None, ctypes.pointer(self._update(jj, l, par)), 1)]
                 if l < L - 1:   # d compressor of layer l+1 (its r arrived one layer ago)
                     items.append(_lib.WgradItem(ctypes.pointer(self._layer(jj, l + 1, par)), _lib.GRAD_COMP, B,
                                                 self.D[jj][cur].data_ptr(), s, self.Y[par][jj][l + 1].data_ptr(), s,
                                                 None, self._received(l + 1, j), None,
-                                                ctypes.pointer(self._update(jj, l + 1, par))))
+                                                ctypes.pointer(self._update(jj, l + 1, par)), 1))
                 per_rank.append(items)
-            if self.bwd_fused and R * (4 if l < L - 1 else 3) <= 15:
-                # r_l first (exposed), then weight gradients + recurrence as ONE LPT-scheduled launch
+
+            def reduce_received():
                 if self.world > 1 and not nvrs:
                     self._join(self.comm_stream, S)
                 if nvrs:
@@ -516,19 +528,19 @@ class PhantomEngine:
                     self._call("ppx_reduce_received", pdt, R, slot, self.world, self.rank, self._pbase + self._soff[l],
                                own, self.Hr[l].data_ptr(), self._pbase + self._rcoff + 4 * l,
                                self._rsepoch[l:].data_ptr(), self.bad.data_ptr(), st)
-                ios = []
-                if l > 0:
-                    for jj in range(R):
-                        j = self.local[jj]
-                        ios.append(self._io(jj, l, par, x=self.D[jj][cur].data_ptr(), ld_x=s,
-                                            out=self.D[jj][1 - cur].data_ptr(), ld_out=s,
-                                            mask=self.Y[par][jj][l].data_ptr() if self.act is Activation.RELU else None,
-                                            ld_m=s, received=self._received(l, j),
-                                            colsum=self.gbias[jj, l - 1].data_ptr()))
-                flat = [it for chunk in per_rank for it in chunk]
-                arr = (_lib.WgradItem * len(flat))(*flat)
-                self._keep.append(arr)
-                self._call("ppx_backward_fused", pdt, len(flat), arr, len(ios), self._ios(ios), B, self.act.code, st)
+
+            if self.bwd_fused:
+                # r_l first (exposed), then weight gradients + recurrence of each group as ONE
+                # LPT-scheduled launch
+                reduce_received()
+                for c0, c1 in self._chunks():
+                    flat = [it for chunk in per_rank[c0:c1] for it in chunk]
+                    ios = [self._recurrence_io(jj, l, par, cur) for jj in range(c0, c1)] if l > 0 else []
+                    arr = (_lib.WgradItem * len(flat))(*flat)
+                    self._keep.append(arr)
+                    self._call("ppx_backward_fused", pdt, len(flat), arr, len(ios), self._ios(ios) if ios else None,
+                               B, self.act.code, st,
+                               flops=sum(self._f_item(it) for it in flat) + len(ios) * self._f_recurrence)
                 if l > 0:
                     cur = 1 - cur
                 continue
@@ -536,41 +548,23 @@ class PhantomEngine:
             per = max(1, min(self.group, 16 // nprob))
             nl = -(-R // per)
             per = -(-R // nl)
-            # leave SMs to the reduce-scatter running on the comm stream under these GEMMs
-            if self.world > 1 and self.comm_sms:
-                self.ctx.call("ppx_set_reserved_sms", self.comm_sms)
             for c in range(0, R, per):
                 self._launch_wgrad([it for chunk in per_rank[c:c + per] for it in chunk], st)
-            if self.world > 1 and self.comm_sms:
-                self.ctx.call("ppx_set_reserved_sms", 0)
-            if self.world > 1 and not nvrs:
-                self._join(self.comm_stream, S)
-            if nvrs:
-                own = self.H[l].data_ptr() + self.rank * R * slot * esz
-                self._call("ppx_reduce_received", pdt, R, slot, self.world, self.rank, self._pbase + self._soff[l], own,
-                           self.Hr[l].data_ptr(), self._pbase + self._rcoff + 4 * l, self._rsepoch[l:].data_ptr(),
-                           self.bad.data_ptr(), st)
+            reduce_received()
             if l > 0:
-                ios = []
-                for jj in range(R):
-                    j = self.local[jj]
-                    ios.append(self._io(jj, l, par, x=self.D[jj][cur].data_ptr(), ld_x=s,
-                                        out=self.D[jj][1 - cur].data_ptr(), ld_out=s,
-                                        mask=self.Y[par][jj][l].data_ptr() if self.act is Activation.RELU else None,
-                                        ld_m=s, received=self._received(l, j),
-                                        colsum=self.gbias[jj, l - 1].data_ptr()))
-                for c in range(0, R, self.group):
-                    self._call("ppx_backward_delta_n", pdt, min(self.group, R - c), self._ios(ios[c:c + self.group]),
-                               B, self.act.code, st)
+                ios = [self._recurrence_io(jj, l, par, cur) for jj in range(R)]
+                for c0, c1 in self._chunks():
+                    self._call("ppx_backward_delta_n", pdt, c1 - c0, self._ios(ios[c0:c1]), B, self.act.code, st,
+                               flops=(c1 - c0) * self._f_recurrence)
                 cur = 1 - cur
         # d compressor of layer 0, all local ranks in one launch
         items = [_lib.WgradItem(ctypes.pointer(self._layer(jj, 0, par)), _lib.GRAD_COMP, B,
                                 self.D[jj][cur].data_ptr(), s, self.Y[par][jj][0].data_ptr(), s, None,
-                                self._received(0, self.local[jj]), None, ctypes.pointer(self._update(jj, 0, par)))
+                                self._received(0, self.local[jj]), None, ctypes.pointer(self._update(jj, 0, par)), 1)
                  for jj in range(R)]
         if self.p > 1:
-            for c in range(0, R, self.group):
-                self._launch_wgrad(items[c:c + self.group], st)
+            for c0, c1 in self._chunks():
+                self._launch_wgrad(items[c0:c1], st)
         # biases of all local ranks and layers in one elementwise launch
         kind = _lib.PPX_UPDATE_ADAM if self.optimizer == "adam" else _lib.PPX_UPDATE_SGD
         self._call("ppx_optimizer_step", kind, self.hyper.data_ptr(), self.bias.data_ptr(), self.gbias.data_ptr(),
@@ -582,7 +576,9 @@ class PhantomEngine:
         self._keep.clear()
         self._launches = 0
         self.trace = []
-        c, st = self.ctx, S.cuda_stream
+        st = S.cuda_stream
+        self._call("ppx_hyper_advance", self.hyper.data_ptr(), self.tdev.data_ptr(), float(self.betas[0]),
+                   float(self.betas[1]), st)
         self._call("ppx_zero", self.gbias.data_ptr(), self.gbias.numel() * 4, st)
         self._call("ppx_zero", self.loss.data_ptr(), 4, st)
         self._forward(par, S)
@@ -592,25 +588,45 @@ class PhantomEngine:
         self.launch_count = self._launches
 
     # ------------------------------------------------------------------------------------------
-    def _set_hyper(self):
-        self.t += 1
-        b1, b2 = self.betas
-        self.hyper_host.copy_(torch.tensor([self.lr, b1, b2, self.eps, 1 - b1 ** self.t, 1 - b2 ** self.t]))
+    def set_lr(self, lr: float):
+        """Change the learning rate between steps (synchronous: graph replays read it from HBM)."""
+        torch.cuda.synchronize()
+        self.lr = lr
+        self.hyper[0] = lr
+        torch.cuda.synchronize()
 
     def step(self, graph: bool = True):
-        """One training iteration on the device-resident batch of the current parity."""
+        """One training iteration on the device-resident batch of the current parity.  Fully
+        asynchronous: nothing on the host is rewritten per step (the Adam step counter lives on
+        the device), so steps may be issued back to back without reading the loss."""
         par = self.parity
         S = torch.cuda.current_stream()
-        self._set_hyper()
-        self.hyper.copy_(self.hyper_host, non_blocking=True)
+        self.t += 1
         if graph and self.graphs[par] is not None:
             self.graphs[par].replay()
         else:
             self._step_body(par, S)
         self.parity = 1 - par
 
+    def profile_step(self):
+        """One eager step with CUDA events around every kernel launch: returns
+        [(abi_call, milliseconds, algorithmic GEMM FLOPs)] in launch order (bench.py's per-kernel
+        roofline)."""
+        self._timing = []
+        try:
+            # hold the stream for ~0.1 s so the host enqueues the whole step before the GPU starts
+            # it: the event pairs then bracket kernels running back to back, never host gaps
+            torch.cuda._sleep(200_000_000)
+            self.step(graph=False)
+            torch.cuda.synchronize()
+            return [(nm, a.elapsed_time(b), f) for nm, a, b, f in self._timing]
+        finally:
+            self._timing = None
+
     def capture(self):
         """Capture one CUDA graph per parity (weights / input double buffers alternate)."""
+        if self.capture_grads:
+            raise ConfigurationError("deltas are recorded by eager steps only: set capture_grads = False first")
         torch.cuda.synchronize()
         for par in (0, 1):
             g = torch.cuda.CUDAGraph()
@@ -627,18 +643,43 @@ class PhantomEngine:
         if self.ctx.handle is None:
             return
         torch.cuda.synchronize()
-        for g in self.graphs:
+        for g in self.graphs + self.infer_graphs:
             if g is not None:
                 g.reset()
         self.graphs = [None, None]
+        self.infer_graphs = [None, None]
         torch.cuda.synchronize()
         self.ctx.close()
 
-    def forward_only(self, par=None):
-        """Inference (config C5): the forward loop without tape, loss or delta."""
+    def forward_only(self, par=None, graph=False):
+        """Inference (config C5; the reference's loop of pp_forward_layer, test_phantom.py:66-71):
+        the forward pass without tape, loss or delta on the input buffers of parity `par`.
+        Returns the [B, s] outputs of this GPU's logical ranks (views, overwritten by the next
+        call).  graph=True replays the inference graph of capture_inference()."""
         par = self.parity if par is None else par
-        self._forward(par, torch.cuda.current_stream(), train=False)
+        if graph and self.infer_graphs[par] is not None:
+            self.infer_graphs[par].replay()
+        else:
+            self._keep.clear()
+            self._launches = 0
+            self._forward(par, torch.cuda.current_stream(), train=False)
+            self.infer_launch_count = self._launches
         return [self.Y[par][jj][self.L] for jj in range(self.R)]
+
+    def capture_inference(self):
+        """Capture the forward-only pass of each parity in a CUDA graph."""
+        torch.cuda.synchronize()
+        for par in (0, 1):
+            g = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream(self.dev)
+            cs.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.graph(g, stream=cs):
+                self._keep.clear()
+                self._launches = 0
+                self._forward(par, torch.cuda.current_stream(), train=False)
+                self.infer_launch_count = self._launches
+            self.infer_graphs[par] = g
+        torch.cuda.synchronize()
 
     # ------------------------------------------------------------------------------------------
     def set_batch(self, x_shards, t_shards, par=None):

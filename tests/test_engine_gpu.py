@@ -1,8 +1,16 @@
 """PhantomEngine (fused epilogues, grouped wgrad with in-place SGD/Adam, CUDA graphs) against
 the pinned CPU oracle: one and several training steps with p logical ranks on one GPU.
 
-fp32 tier tolerance 1e-4 (normwise); bf16 tier: loss 2e-2, weights after the step 2e-2.
+Every test compares the losses and the weight UPDATES W_T - W_0 of every tensor (local,
+compressor, each decompressor, bias) with the oracle's: a zero, dropped or misplaced gradient moves
+its update by ~100%.  fp32 tier 1e-4 (normwise).  bf16 tier: losses 2e-2; SGD updates 1e-1 and
+Adam updates 2.5e-1 — against the float64 oracle the bf16 activations perturb every gradient by a
+few 1e-2 over three ReLU layers at width 512 (the per-kernel bf16 arithmetic itself is checked
+teacher-forced at 5e-3 in test_parity_scale_gpu.py), and Adam's m / sqrt(v) turns the relative
+noise of near-zero gradient entries into O(1) noise of their updates.
 """
+import copy
+
 import numpy as np
 import pytest
 import torch
@@ -19,7 +27,7 @@ def nerr(a, b):
     return float(np.linalg.norm(a - b) / (d if d > 0 else 1.0))
 
 
-def _setup(n, p, k, L, B, dtype, optimizer, lr, seed=3, act="relu"):
+def _setup(n, p, k, L, B, dtype, optimizer, lr, seed=3, act="relu", **kw):
     from paper_2508_00960_b200.engine import PhantomEngine
     model = po.init_phantom_model(n, p, k, L, seed)
     rng = np.random.default_rng(seed)
@@ -28,7 +36,7 @@ def _setup(n, p, k, L, B, dtype, optimizer, lr, seed=3, act="relu"):
             lay["bias"] = 0.1 * rng.standard_normal(lay["bias"].shape)
     x = rng.standard_normal((n, B))
     y = np.maximum(rng.standard_normal((n, B)), 0.0)
-    eng = PhantomEngine(n, p, k, L, B, optimizer=optimizer, lr=lr, dtype=dtype, activation=act)
+    eng = PhantomEngine(n, p, k, L, B, optimizer=optimizer, lr=lr, dtype=dtype, activation=act, **kw)
     eng.load_params(model)
     s = n // p
     xs = [torch.from_numpy(x[j * s:(j + 1) * s].T.copy()).cuda() for j in range(p)]
@@ -36,6 +44,22 @@ def _setup(n, p, k, L, B, dtype, optimizer, lr, seed=3, act="relu"):
     for par in (0, 1):
         eng.set_batch(xs, ys, par)
     return eng, model, x, y
+
+
+def _check_updates(eng, model0, model, tol):
+    """normwise error of the engine's update of every parameter tensor vs the oracle's update."""
+    worst = 0.0
+    for jj, j in enumerate(eng.local):
+        for l in range(eng.L):
+            v = eng.layer_views(jj, l)
+            pairs = [(v[nm], model0[j][l][nm], model[j][l][nm]) for nm in ("local", "compressor", "bias")]
+            pairs += [(d, model0[j][l]["decompressors"][i], model[j][l]["decompressors"][i])
+                      for i, d in v["decompressors"].items()]
+            for got, w0, w1 in pairs:
+                e = nerr(got.double().cpu().numpy() - w0, w1 - w0)
+                worst = max(worst, e)
+    assert worst <= tol, worst
+    return worst
 
 
 def _oracle_steps(model, x, y, L, steps, optimizer, lr, act="relu"):
@@ -65,6 +89,7 @@ def test_engine_steps_match_oracle(dtype, tol, optimizer, graph):
     n, p, k, L, B = 512, 4, 32, 3, 64
     lr = 3e-3 if optimizer == "sgd" else 1e-3
     eng, model, x, y = _setup(n, p, k, L, B, dtype, optimizer, lr)
+    model0 = copy.deepcopy(model)
     steps = 3
     if graph:
         eng.capture()
@@ -75,14 +100,25 @@ def test_engine_steps_match_oracle(dtype, tol, optimizer, graph):
     ref = _oracle_steps(model, x, y, L, steps, optimizer, lr)
     for a, b in zip(losses, ref):
         assert abs(a - b) <= tol * abs(b), (losses, ref)
-    for jj in range(p):
-        for l in range(L):
-            v = eng.layer_views(jj, l)
-            assert nerr(v["local"], model[jj][l]["local"]) <= tol
-            assert nerr(v["compressor"], model[jj][l]["compressor"]) <= tol
-            assert nerr(v["bias"], model[jj][l]["bias"]) <= tol
-            for i, d in v["decompressors"].items():
-                assert nerr(d, model[jj][l]["decompressors"][i]) <= tol
+    _check_updates(eng, model0, model, tol if dtype == torch.float32 else (1e-1 if optimizer == "sgd" else 2.5e-1))
+
+
+@pytest.mark.parametrize("optimizer", ["adam", "sgd"])
+def test_engine_unsynchronised_graph_replays(optimizer):
+    """Five CUDA-graph steps issued back to back with no host synchronisation in between (the
+    bench's timing loop): the Adam bias corrections 1 - beta^t are advanced on the device, so
+    every step uses its own t (training.py:92-105) — fp32 tier vs the oracle at 1e-4."""
+    n, p, k, L, B = 512, 4, 32, 3, 64
+    lr = 1e-3 if optimizer == "adam" else 3e-3
+    eng, model, x, y = _setup(n, p, k, L, B, torch.float32, optimizer, lr)
+    model0 = copy.deepcopy(model)
+    eng.capture()
+    for _ in range(5):
+        eng.step()
+    loss = eng.read_loss()
+    ref = _oracle_steps(model, x, y, L, 5, optimizer, lr)
+    assert abs(loss - ref[-1]) <= 1e-4 * abs(ref[-1]), (loss, ref)
+    _check_updates(eng, model0, model, 1e-4)
 
 
 def test_engine_forward_only_matches_oracle():
@@ -97,13 +133,13 @@ def test_engine_forward_only_matches_oracle():
 
 
 @pytest.mark.parametrize("graph", [False, True])
-def test_engine_fused_forward_matches_oracle(graph, monkeypatch):
-    """PPX_FUSED=1: compression + (in-kernel) phantom exchange + forward of each layer as ONE
+def test_engine_fused_forward_matches_oracle(graph):
+    """fused=True: compression + (in-kernel) phantom exchange + forward of each layer as ONE
     2-SM launch (forward tiles wait on the compression tiles' arrival counter) — bf16 steps
     against the float64 oracle."""
-    monkeypatch.setenv("PPX_FUSED", "1")
     n, p, k, L, B, lr = 512, 4, 64, 3, 256, 3e-3
-    eng, model, x, y = _setup(n, p, k, L, B, torch.bfloat16, "sgd", lr)
+    eng, model, x, y = _setup(n, p, k, L, B, torch.bfloat16, "sgd", lr, fused=True)
+    model0 = copy.deepcopy(model)
     assert eng.fused
     if graph:
         eng.capture()
@@ -114,11 +150,7 @@ def test_engine_fused_forward_matches_oracle(graph, monkeypatch):
     ref = _oracle_steps(model, x, y, L, 3, "sgd", lr)
     for a, b in zip(losses, ref):
         assert abs(a - b) <= 2e-2 * abs(b), (losses, ref)
-    for jj in range(p):
-        for l in range(L):
-            v = eng.layer_views(jj, l)
-            assert nerr(v["local"], model[jj][l]["local"]) <= 2e-2
-            assert nerr(v["compressor"], model[jj][l]["compressor"]) <= 2e-2
+    _check_updates(eng, model0, model, 1e-1)
 
 
 @pytest.mark.parametrize("graph", [False, True])
@@ -126,7 +158,8 @@ def test_engine_pair_kernel_matches_oracle(graph):
     """64-aligned s and k: every contraction runs on the 2-SM kernel (spanning phantom-slot tiles,
     M < 256 weight-gradient problems) — bf16 steps against the float64 oracle."""
     n, p, k, L, B, lr = 512, 4, 64, 3, 256, 3e-3
-    eng, model, x, y = _setup(n, p, k, L, B, torch.bfloat16, "sgd", lr)
+    eng, model, x, y = _setup(n, p, k, L, B, torch.bfloat16, "sgd", lr, fused=False)
+    model0 = copy.deepcopy(model)
     if graph:
         eng.capture()
     losses = []
@@ -136,16 +169,17 @@ def test_engine_pair_kernel_matches_oracle(graph):
     ref = _oracle_steps(model, x, y, L, 3, "sgd", lr)
     for a, b in zip(losses, ref):
         assert abs(a - b) <= 2e-2 * abs(b), (losses, ref)
+    _check_updates(eng, model0, model, 1e-1)
 
 
 @pytest.mark.parametrize("p", [2, 4])
 @pytest.mark.parametrize("graph", [False, True])
-def test_engine_backward_fused_matches_oracle(graph, p, monkeypatch):
-    """PPX_BWD_FUSED=1: weight gradients (+ fused SGD) and the error recurrence of each layer as ONE
+def test_engine_backward_fused_matches_oracle(graph, p):
+    """bwd_fused=True (group=1): weight gradients (+ fused SGD) and the error recurrence of each layer as ONE
     launch with a static longest-first tile schedule — bf16 steps against the float64 oracle."""
-    monkeypatch.setenv("PPX_BWD_FUSED", "1")
     n, k, L, B, lr = 128 * p, 64, 3, 256, 3e-3
-    eng, model, x, y = _setup(n, p, k, L, B, torch.bfloat16, "sgd", lr)
+    eng, model, x, y = _setup(n, p, k, L, B, torch.bfloat16, "sgd", lr, group=1)
+    model0 = copy.deepcopy(model)
     assert eng.bwd_fused
     if graph:
         eng.capture()
@@ -156,9 +190,4 @@ def test_engine_backward_fused_matches_oracle(graph, p, monkeypatch):
     ref = _oracle_steps(model, x, y, L, 3, "sgd", lr)
     for a, b in zip(losses, ref):
         assert abs(a - b) <= 2e-2 * abs(b), (losses, ref)
-    for jj in range(p):
-        for l in range(L):
-            v = eng.layer_views(jj, l)
-            assert nerr(v["local"], model[jj][l]["local"]) <= 2e-2
-            for i, d in v["decompressors"].items():
-                assert nerr(d, model[jj][l]["decompressors"][i]) <= 2e-2
+    _check_updates(eng, model0, model, 1e-1)

@@ -1,0 +1,99 @@
+"""Multi-GPU parity of the tensor-parallel comparison pipeline: TPEngine (Megatron column/row
+pairs, NCCL all-reduces) on N GPUs (torchrun, one process per GPU) vs the dense float64 oracle —
+TP is an exact reparameterisation of the dense FFN (reference tensor_parallel.py:67-153,
+training.py:216-244; test_acceptance.py:100-118).
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/mp_tp_parity.py [--dtype fp32|bf16]
+
+Compares every step's loss and each GPU's weight UPDATES (its row block of the column-parallel
+layers, its column block of the row-parallel layers, both biases) with the oracle's.
+Tolerances: fp32 tier 1e-4; bf16 tier 2e-2 losses, 5e-2 updates.  Rank 0 prints one JSON verdict.
+"""
+import argparse, json, os, sys
+import numpy as np
+import torch
+import torch.distributed as dist
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from oracle import phantom_oracle as po
+from paper_2508_00960_b200 import _lib
+from paper_2508_00960_b200.tensor_parallel import TPEngine
+
+
+def nerr(a, b):
+    d = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / (d if d > 0 else 1.0))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--dtype", default="fp32")
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--width", type=int, default=512)
+    ap.add_argument("--layers", type=int, default=4)
+    ap.add_argument("--B", type=int, default=64)
+    ap.add_argument("--lr", type=float, default=3e-3)
+    args = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    uid = [_lib.Context.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    n, L, B, lr = args.width, args.layers, args.B, args.lr
+    f32 = args.dtype == "fp32"
+    dtype = torch.float32 if f32 else torch.bfloat16
+    tol_l, tol_u = (1e-4, 1e-4) if f32 else (2e-2, 5e-2)
+    rng = np.random.default_rng(5)
+    a = np.sqrt(6.0 / (2 * n))
+    W = [rng.uniform(-a, a, (n, n)) for _ in range(L)]
+    b = [0.1 * rng.standard_normal(n) for _ in range(L)]
+    x = rng.standard_normal((n, B))
+    y = np.maximum(rng.standard_normal((n, B)), 0.0)
+    eng = TPEngine(n, L, B, world=world, rank=rank, device=local, uid=uid[0], lr=lr, dtype=dtype)
+    eng.load_full_weights(W, b)
+    for par in (0, 1):
+        eng.set_batch(torch.from_numpy(x.T.copy()).cuda(), torch.from_numpy(y.T.copy()).cuda(), par)
+    losses = []
+    eng.step(graph=False)
+    losses.append(eng.read_loss())
+    eng.capture()
+    for _ in range(args.steps - 1):
+        eng.step()
+        losses.append(eng.read_loss())
+    Wd = [w.copy() for w in W]
+    bd = [v.copy() for v in b]
+    ref = []
+    for _ in range(args.steps):
+        out = po.tp_iteration([[{"weight": Wd[l], "bias": bd[l]} for l in range(L)]], ["relu"] * L, [x], [y], "mean")
+        ref.append(out["global_loss"])
+        for l in range(L):
+            Wd[l] -= lr * out["grads"][0][l]["weight"]
+            bd[l] -= lr * out["grads"][0][l]["bias"]
+    s = n // world
+    r0, r1 = rank * s, (rank + 1) * s
+    worst = {"loss": max(abs(g - r) / abs(r) for g, r in zip(losses, ref)), "update": 0.0}
+    for m in range(L // 2):
+        upd = [(eng.Wa[m], W[2 * m][r0:r1, :], Wd[2 * m][r0:r1, :]),
+               (eng.Wb[m], W[2 * m + 1][:, r0:r1], Wd[2 * m + 1][:, r0:r1]),
+               (eng._ba(m), b[2 * m][r0:r1], bd[2 * m][r0:r1]),
+               (eng._bb(m), b[2 * m + 1], bd[2 * m + 1])]
+        for got, w0, w1 in upd:
+            worst["update"] = max(worst["update"], nerr(got.double().cpu().numpy() - w0, w1 - w0))
+    w = torch.tensor([worst["loss"], worst["update"]], device="cuda", dtype=torch.float64)
+    dist.all_reduce(w, op=dist.ReduceOp.MAX)
+    ok = bool(w[0] <= tol_l and w[1] <= tol_u)
+    if rank == 0:
+        print(json.dumps({"world": world, "dtype": args.dtype, "losses": losses, "oracle": ref,
+                          "worst": {"loss": float(w[0]), "update": float(w[1])},
+                          "tol": {"loss": tol_l, "update": tol_u}, "pass": ok}), flush=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    eng.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.stdout.flush()
+    os._exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,5 +1,5 @@
 """Per-ABI-call device time of one eager PhantomEngine step on N GPUs (torchrun), from CUDA events
-recorded around every call on the stream it was issued to.  Rank 0 prints per-call totals and
+recorded around every kernel launch (PhantomEngine.profile_step).  Rank 0 prints per-call totals and
 the wall of the step.   torchrun --nproc-per-node N tools/mp_trace.py [--config c3]"""
 import argparse, collections, json, os, sys
 import torch
@@ -31,33 +31,22 @@ eng.set_batch(xs, ts, 1)
 for _ in range(2):
     eng.step(graph=False)
 torch.cuda.synchronize()
-recs = []
-orig = eng._call
-def traced(name, *a):
-    st = a[-1]
-    s = torch.cuda.ExternalStream(st) if isinstance(st, int) and st else torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(s)
-    orig(name, *a)
-    e1.record(s)
-    recs.append((name, e0, e1))
-eng._call = traced
 if world > 1:
     dist.barrier()
 torch.cuda.synchronize()
 S = torch.cuda.current_stream()
 t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 t0.record(S)
-eng.step(graph=False)
+seq = eng.profile_step()
 t1.record(S)
 torch.cuda.synchronize()
 agg = collections.OrderedDict()
-for name, a, b in recs:
+for name, ms in seq:
     x = agg.setdefault(name, [0, 0.0])
     x[0] += 1
-    x[1] += a.elapsed_time(b) * 1e3
+    x[1] += ms * 1e3
 out = {"rank": rank, "step_us": t0.elapsed_time(t1) * 1e3, "calls": {k: [v[0], round(v[1], 1)] for k, v in agg.items()},
-       "seq": [(n, round(a.elapsed_time(b) * 1e3, 1)) for n, a, b in recs]}
+       "seq": [(n, round(ms * 1e3, 1)) for n, ms in seq]}
 outs = [None] * world
 if world > 1:
     dist.all_gather_object(outs, out)
