@@ -166,12 +166,18 @@ def reference_steps(n, p, k, layers, batch, steps, warmup):
                 out = ps.pp_iteration(comm, rank, model[rank], acts, xs[rank], ys[rank], "mean")
                 params, grads, names = _pp_param_lists(model[rank], out.grads)
                 ps.sgd_step(params, grads, 1e-4, names=names)
+        # one host thread per rank (the reference's "threads" scheduler), each BLAS call on
+        # cores // p threads: the fastest setting measured for this reference (8-core host, C3:
+        # 0.76 s/step vs 1.49 lockstep with all cores per call, 1.77 threads oversubscribed)
+        per = max(1, cores // p)
         comm = ps.Communicator(p, mode="threads", timeout=3600.0)
-        if warmup:
-            comm.run(worker, warmup)
-        t0 = time.perf_counter()
-        comm.run(worker, steps)
-        return (time.perf_counter() - t0) / steps, "reference", cores
+        with _blas_threads(per):
+            if warmup:
+                comm.run(worker, warmup)
+            t0 = time.perf_counter()
+            comm.run(worker, steps)
+            dt = (time.perf_counter() - t0) / steps
+        return dt, "reference", per * p
     from oracle import phantom_oracle as po
     model = [[{"local": rng.uniform(-a, a, (s, s)), "compressor": rng.uniform(-a, a, (k, s)),
                "decompressors": {i: rng.uniform(-a, a, (s, k)) for i in range(p) if i != j}, "bias": np.zeros(s)}
@@ -182,20 +188,30 @@ def reference_steps(n, p, k, layers, batch, steps, warmup):
         for j in range(p):
             params, gs = po.pp_param_list(model[j], out["grads"][j])
             po.sgd_step(params, gs, 1e-4)
-    for _ in range(warmup):
-        one()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        one()
-    return (time.perf_counter() - t0) / steps, "port", cores
+    with _blas_threads(cores):
+        for _ in range(warmup):
+            one()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            one()
+        dt = (time.perf_counter() - t0) / steps
+    return dt, "port", cores
+
+
+def _blas_threads(n):
+    """Limit the BLAS pool at run time (numpy may already be loaded, so env vars are too late)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=n, user_api="blas")
+    except Exception:  # pragma: no cover
+        import contextlib
+        return contextlib.nullcontext()
 
 
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cores = os.cpu_count() or 1
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
     n, p, k, L = cfg["n"], cfg["p"], cfg["k"], cfg["layers"]
     sample_b = 256
     sample_l = L if n <= 16384 else 1   # C4's float64 weights do not fit host RAM: one layer, x L
@@ -221,14 +237,13 @@ def run_reference(args, cfg):
 def cpu_baseline(args, cfg):
     """The reference on this box's host cores, one layer of the model at batch 256, scaled to L."""
     cores = os.cpu_count() or 1
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
     n, p, k, L = cfg["n"], cfg["p"], cfg["k"], cfg["layers"]
     sample_b = 256
     try:
         dt, kind, threads = reference_steps(n, p, k, 1, sample_b, 2, 1)
         return {"value": sample_b / (dt * L), "unit": "samples/s", "cores": threads, "kind": kind,
                 "sample": f"{'phantomsim' if kind == 'reference' else 'oracle port'} pp_iteration + sgd_step "
-                          f"(float64, numpy/OpenBLAS, {threads} threads) of ONE layer of the {args.config} model "
+                          f"(float64, numpy/OpenBLAS, {threads} threads in all) of ONE layer of the {args.config} model "
                           f"(all {p} ranks) at batch {sample_b}, mean of 2 after 1 warm-up, scaled x{L} layers"}
     except Exception as exc:  # pragma: no cover
         return {"value": None, "unit": "samples/s", "cores": cores, "kind": "reference", "sample": f"failed: {exc}"}

@@ -292,7 +292,7 @@ def load_state(path, eng) -> int:
             raise ConfigurationError(f"{side}: bad magic {magic!r}")
         if (kind == 1) != (eng.optimizer == "adam"):
             raise ConfigurationError(f"{side}: optimizer kind does not match the engine")
-        eng.t = int(t)
+        eng.set_step_count(int(t))
         if kind == 1:
             if per_moment != geo.block_elems * geo.p * geo.layers:
                 raise ConfigurationError(f"{side}: moment size does not match the engine")

@@ -8,12 +8,34 @@
 
 from __future__ import annotations
 
+import math
+import zlib
 from enum import Enum
 
+import numpy as np
 import torch
 
 from . import _lib, kernels
 from .errors import ConfigurationError
+
+
+def _key_word(part) -> int:
+    """One spawn-key word: strings hash through CRC-32, integers keep their low 32 bits."""
+    return zlib.crc32(part.encode("utf-8")) if isinstance(part, str) else int(part) & 0xFFFFFFFF
+
+
+def substream(seed: int, *key) -> np.random.Generator:
+    """core.py:101-114 — an independent Philox stream per (seed, *key): SeedSequence(seed) with
+    the key as spawn key, two 64-bit words of its state as the Philox key.  Host-side: model
+    construction must reproduce the reference's draws bit for bit."""
+    seq = np.random.SeedSequence(entropy=int(seed) & (2**63 - 1), spawn_key=tuple(_key_word(x) for x in key))
+    return np.random.Generator(np.random.Philox(key=seq.generate_state(2, dtype=np.uint64)))
+
+
+def uniform_init(rng: np.random.Generator, rows: int, cols: int, fan_in: int, fan_out: int) -> np.ndarray:
+    """core.py:117-125 — Glorot-uniform U[-a, a], a = sqrt(6 / (fan_in + fan_out)), float64."""
+    bound = math.sqrt(6.0 / (fan_in + fan_out))
+    return rng.uniform(-bound, bound, size=(rows, cols))
 
 
 class FlopCounter:

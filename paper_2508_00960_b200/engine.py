@@ -588,6 +588,13 @@ class PhantomEngine:
         self.launch_count = self._launches
 
     # ------------------------------------------------------------------------------------------
+    def set_step_count(self, t: int):
+        """Set the optimizer step counter (Adam's t; the next step uses t + 1), e.g. on resume."""
+        torch.cuda.synchronize()
+        self.t = int(t)
+        self.tdev.fill_(int(t))
+        torch.cuda.synchronize()
+
     def set_lr(self, lr: float):
         """Change the learning rate between steps (synchronous: graph replays read it from HBM)."""
         torch.cuda.synchronize()

@@ -20,7 +20,8 @@ import torch
 
 from . import _lib, kernels
 from .collectives import Communicator, Direction
-from .core import Activation, FlopCounter, as_activation, flat_offsets, round8, row_major
+from .core import (Activation, FlopCounter, as_activation, flat_offsets, round8, row_major, substream,
+                   uniform_init)
 from .errors import ConfigurationError, SequencingError
 
 DEFAULT_DTYPE = torch.bfloat16
@@ -174,26 +175,11 @@ class PhantomModel:
 # model construction
 # ----------------------------------------------------------------------------------------------
 def _reference_init_arrays(n, p, k, layers, seed, j, l):
-    """The reference's seeded Glorot-uniform draws (phantom.py:126-129 via core.py:101-125),
-    reproduced bit-for-bit with numpy's Philox on the host."""
-    import math
-    import zlib
-
-    def key_part(x):
-        return zlib.crc32(x.encode()) if isinstance(x, str) else int(x) & 0xFFFFFFFF
-
-    def stream(*key):
-        ss = np.random.SeedSequence(entropy=int(seed) & (2**63 - 1), spawn_key=tuple(key_part(x) for x in key))
-        return np.random.Generator(np.random.Philox(key=ss.generate_state(2, dtype=np.uint64)))
-
-    def uni(rng, rows, cols, fi, fo):
-        a = math.sqrt(6.0 / (fi + fo))
-        return rng.uniform(-a, a, size=(rows, cols))
-
+    """The reference's seeded Glorot-uniform draws (phantom.py:126-129), bit-for-bit on the host."""
     s = n // p
-    local = uni(stream("pp", l, j, "local"), s, s, s, s)
-    comp = uni(stream("pp", l, j, "compressor"), k, s, s, k)
-    decs = {i: uni(stream("pp", l, j, "decompressor", i), s, k, k, s) for i in range(p) if i != j}
+    local = uniform_init(substream(seed, "pp", l, j, "local"), s, s, s, s)
+    comp = uniform_init(substream(seed, "pp", l, j, "compressor"), k, s, s, k)
+    decs = {i: uniform_init(substream(seed, "pp", l, j, "decompressor", i), s, k, k, s) for i in range(p) if i != j}
     return local, comp, decs
 
 
@@ -443,6 +429,25 @@ def pp_param_grads(layer: PhantomLayer, delta, tape_entry: LayerTape, received_p
     if counter is not None:
         counter.add(2 * s * s * B + 2 * k * s * B + (p - 1) * 2 * s * k * B + s * B)
     return grads_from_flat(flat, s, k, p, layer.rank)
+
+
+def effective_weight(model: PhantomModel, layer_index: int) -> torch.Tensor:
+    """reference.py:143-157 — the dense n x n matrix a phantom layer applies: diagonal block j is
+    local_j, block (row j, col i) is decompressor_{i->j} . compressor_i (rank <= k), built on the
+    model's device in fp32 (a verification helper for the layout invariant of SURVEY §8e, not on
+    the training path)."""
+    if not 0 <= layer_index < model.layer_count:
+        raise ConfigurationError(f"layer {layer_index} out of range")
+    s, p = model.shard_width, model.p
+    first = model.rank_layers[0][layer_index].local
+    W = torch.zeros((model.n, model.n), dtype=torch.float32, device=first.device)
+    for j in range(p):
+        lay = model.rank_layers[j][layer_index]
+        W[j * s:(j + 1) * s, j * s:(j + 1) * s] = lay.local.float()
+        for i, dec in lay.decompressors.items():
+            comp = model.rank_layers[i][layer_index].compressor
+            W[j * s:(j + 1) * s, i * s:(i + 1) * s] = dec.float() @ comp.float()
+    return W
 
 
 def pp_model_size(n: int, p: int, k: int, layers: int) -> int:

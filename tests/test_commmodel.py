@@ -47,3 +47,40 @@ def test_time_and_errors():
     with pytest.raises(FitError):
         fit_comm_model([(Collective.ALL_GATHER, 1, 2, 1.0), (Collective.ALL_GATHER, 2, 2, 2.0),
                         (Collective.ALL_GATHER, 3, 2, 3.0)])
+
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not __import__("os").path.isdir(REF_SRC), reason="reference tree not present")
+@pytest.mark.parametrize("seed", range(4))
+def test_fit_matches_reference_fitter(seed):
+    """Same coefficients as phantomsim's fit_comm_model (lstsq, then scipy lsq_linear with the
+    bounds when c1 or c2 come out negative) on noisy samples, some with a falling latency term."""
+    import sys
+    import numpy as np
+    sys.path.insert(0, REF_SRC)
+    from phantomsim import collectives as ref
+    rng = np.random.default_rng(seed)
+    samples = []
+    for kind in Collective:
+        c1 = rng.uniform(-5.0, 20.0) if seed % 2 else rng.uniform(0.0, 20.0)
+        for p in (2, 4, 8):
+            for m in (4, 1 << 10, 1 << 16, 1 << 22):
+                samples.append((kind, m, p, max(0.5, c1 * math.log2(p) + 2e-5 * m + 8.0 + rng.normal(0, 2.0))))
+    ours = fit_comm_model(samples)
+    theirs = ref.fit_comm_model([(k.value, m, p, t) for k, m, p, t in samples])
+    for kind in Collective:
+        a, b = ours.costs[kind], theirs.costs[ref.Collective(kind.value)]
+        assert (a.c1, a.c2, a.c3) == pytest.approx((b.c1, b.c2, b.c3), rel=1e-6, abs=1e-9)
+        assert ours.rmse_log2_us[kind] == pytest.approx(theirs.rmse_log2_us[ref.Collective(kind.value)], abs=1e-9)
+
+
+@pytest.mark.skipif(not __import__("os").path.isdir(REF_SRC), reason="reference tree not present")
+def test_reads_reference_default_model(tmp_path):
+    """The reference's shipped Frontier constants (data/default_comm_model.ini) load unchanged and
+    survive a save/load round trip."""
+    m = load_comm_model(REF_SRC + "/phantomsim/data/default_comm_model.ini")
+    assert m.costs[Collective.ALL_GATHER].c1 == 149.94 and m.rmse_log2_us[Collective.REDUCE_SCATTER] == 3.91
+    save_comm_model(m, tmp_path / "x.ini")
+    assert load_comm_model(tmp_path / "x.ini").costs == m.costs

@@ -162,3 +162,28 @@ def test_c1_iteration_fp32_tier_vs_oracle():
             for i in gr["decompressors"]:
                 assert nerr(g.decompressors[i], gr["decompressors"][i]) <= 1e-4
             assert nerr(outs[r].deltas[l], ref["deltas"][r][l]) <= 1e-4
+
+
+@pytest.mark.parametrize("mode", ["lockstep", "threads"])
+def test_effective_weight_and_schedulers(mode):
+    """reference.py:143-157 effective weight (block (j, i) = D_{i->j} . C_i) of the reference-init
+    model vs the oracle, and one pp_iteration under both schedulers of the Communicator (the
+    reference default is lockstep): identical results and record streams."""
+    import paper_2508_00960_b200 as ps
+    n, p, k, L, B = 64, 4, 3, 2, 5
+    model = ps.init_phantom_model(n, p, k, L, seed=4, dtype=torch.float32)
+    ref_model = po.init_phantom_model(n, p, k, L, 4)
+    for l in range(L):
+        assert nerr(ps.effective_weight(model, l), po.effective_weight(ref_model, l)) <= 1e-6
+    rng = np.random.default_rng(0)
+    x = torch.from_numpy(rng.standard_normal((n, B))).cuda().float()
+    y = torch.from_numpy(np.maximum(rng.standard_normal((n, B)), 0)).cuda().float()
+    s = n // p
+    comm = ps.Communicator(p, mode=mode)
+    outs = comm.run(lambda c, r: ps.pp_iteration(c, r, model.rank_layers[r], model.activations,
+                                                 x[r * s:(r + 1) * s], y[r * s:(r + 1) * s], "mean"))
+    ref = po.pp_iteration(ref_model, ["relu"] * L, [x[r * s:(r + 1) * s].double().cpu().numpy() for r in range(p)],
+                          [y[r * s:(r + 1) * s].double().cpu().numpy() for r in range(p)], "mean")
+    assert outs[0].global_loss == pytest.approx(ref["global_loss"], rel=1e-4)
+    kinds = [(r.collective.value, r.message_size) for r in comm.records]
+    assert kinds == [("all_gather", k * B)] * L + [("all_reduce", 1)] + [("reduce_scatter", k * B)] * L

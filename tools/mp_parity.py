@@ -7,7 +7,13 @@ Each process owns p/N logical ranks.  Step 1 runs eagerly with the raw fp32 weig
 captured and compares them (local, compressor, every decompressor, bias) with the oracle's
 step-1 gradients; steps 2..S replay CUDA graphs; then the losses and the weight UPDATES W_S - W_0
 of every tensor are compared with the oracle's.  Rank 0 prints one JSON verdict (max over ranks).
-Tolerances: fp32 tier 1e-4; bf16 tier 3e-2 gradients, 5e-2 updates, 2e-2 losses.
+Then every process re-runs the same steps with a one-GPU engine holding all p logical ranks (the
+launch plan parity-tested kernel by kernel in tests/test_parity_scale_gpu.py) and compares the
+same quantities with it: that isolates what the multi-GPU exchange adds.
+Tolerances vs the float64 oracle: fp32 tier 1e-4 gradients and losses, 1e-3 updates (the fp32
+master's rounding, eps32 * |W|, is ~1e-3 of a 3-step update); bf16 tier 1e-1 gradients and
+updates (bf16 activations over 3 ReLU layers), 2e-2 losses.  vs the one-GPU engine: fp32 1e-4,
+bf16 2e-2.
 """
 import argparse, copy, json, os, sys
 import numpy as np
@@ -26,6 +32,47 @@ def nerr(a, b):
 
 def tri(v):
     return None if v == "auto" else v == "1"
+
+
+def snapshot(eng, master):
+    """{(j, l): {local, compressor, bias, decompressors{i}}} as float64 numpy of the flat tensor
+    `master` (eng.master or eng.grad; bias from eng.bias / eng.gbias)."""
+    out = {}
+    for jj, j in enumerate(eng.local):
+        for l in range(eng.L):
+            v = eng.layer_views(jj, l, master=master[jj, l],
+                                bias=(eng.gbias if master is eng.grad else eng.bias)[jj, l])
+            out[(j, l)] = {nm: v[nm].double().cpu().numpy().copy() for nm in ("local", "compressor", "bias")}
+            out[(j, l)]["decompressors"] = {i: d.double().cpu().numpy().copy() for i, d in v["decompressors"].items()}
+    return out
+
+
+def run_engine(eng, model, x, y, args):
+    """load the model + batch, step 1 eager with raw gradients captured, steps 2..S (graphs)."""
+    n, p, s = eng.n, eng.p, eng.s
+    eng.load_params(model)
+    xs = [torch.from_numpy(x[j * s:(j + 1) * s].T.copy()).cuda() for j in eng.local]
+    ys = [torch.from_numpy(y[j * s:(j + 1) * s].T.copy()).cuda() for j in eng.local]
+    eng.set_batch(xs, ys, 0)
+    eng.set_batch(xs, ys, 1)
+    losses = []
+    eng.step(graph=False)
+    losses.append(eng.read_loss())
+    grads = snapshot(eng, eng.grad)
+    eng.capture_grads = False
+    if args.graph:
+        eng.capture()
+    for _ in range(args.steps - 1):
+        eng.step(graph=bool(args.graph))
+        losses.append(eng.read_loss())
+    return losses, grads, snapshot(eng, eng.master)
+
+
+def tensors(d):
+    for nm in ("local", "compressor", "bias"):
+        yield nm, d[nm]
+    for i, t in sorted(d["decompressors"].items()):
+        yield f"dec{i}", t
 
 
 def main():
@@ -52,39 +99,31 @@ def main():
     n, p, k, L, B, lr = args.width, args.p, args.k, args.layers, args.B, args.lr
     dtype = torch.float32 if args.dtype == "fp32" else torch.bfloat16
     f32 = args.dtype == "fp32"
-    tol_g, tol_u, tol_l = (1e-4, 1e-4, 1e-4) if f32 else (3e-2, 5e-2, 2e-2)
+    tol_g, tol_u, tol_l = (1e-4, 1e-3, 1e-4) if f32 else (1e-1, 1e-1, 2e-2)
+    tol_e = 1e-4 if f32 else 2e-2
     model = po.init_phantom_model(n, p, k, L, 3)
     rng = np.random.default_rng(3)
     for row in model:
         for lay in row:
             lay["bias"] = 0.1 * rng.standard_normal(lay["bias"].shape)
     model0 = copy.deepcopy(model)
+    s = n // p
     x = rng.standard_normal((n, B))
     y = np.maximum(rng.standard_normal((n, B)), 0.0)
     eng = PhantomEngine(n, p, k, L, B, world=world, rank=rank, device=local, uid=uid[0], lr=lr, dtype=dtype,
                         fused=tri(args.fused), nvrs=tri(args.nvrs), capture=True)
-    eng.load_params(model)
-    s = n // p
-    xs = [torch.from_numpy(x[j * s:(j + 1) * s].T.copy()).cuda() for j in eng.local]
-    ys = [torch.from_numpy(y[j * s:(j + 1) * s].T.copy()).cuda() for j in eng.local]
-    eng.set_batch(xs, ys, 0)
-    eng.set_batch(xs, ys, 1)
     if args.infer:
         return infer(args, eng, model, x, rank, world, s, p, L, tol_l)
-    losses = []
-    eng.step(graph=False)                     # step 1: raw gradients captured
-    losses.append(eng.read_loss())
-    grads = [[{nm: t.double().cpu().numpy().copy() for nm, t in eng.layer_views(jj, l, master=eng.grad[jj, l]).items()
-               if nm != "decompressors"} | {"decompressors": {i: d.double().cpu().numpy().copy() for i, d in
-                                                              eng.layer_views(jj, l, master=eng.grad[jj, l])["decompressors"].items()},
-                                            "bias": eng.gbias[jj, l].double().cpu().numpy().copy()}
-              for l in range(L)] for jj in range(eng.R)]
-    eng.capture_grads = False
-    if args.graph:
-        eng.capture()
-    for _ in range(args.steps - 1):
-        eng.step(graph=bool(args.graph))
-        losses.append(eng.read_loss())
+    losses, grads, weights = run_engine(eng, model, x, y, args)
+    plan = {"fused": bool(eng.fused), "nvrs": bool(eng.nvrs), "bwd_fused": bool(eng.bwd_fused)}
+    local_ranks = list(eng.local)
+    torch.cuda.synchronize()
+    dist.barrier()
+    eng.close()
+    # the same steps on ONE GPU holding all p logical ranks
+    one = PhantomEngine(n, p, k, L, B, lr=lr, dtype=dtype, device=local, capture=True)
+    losses1, grads1, weights1 = run_engine(one, model, x, y, args)
+    one.close()
     ref, ref_grads = [], None
     for t in range(args.steps):
         out = po.pp_iteration(model, ["relu"] * L, [x[j * s:(j + 1) * s] for j in range(p)],
@@ -95,32 +134,33 @@ def main():
         for j in range(p):
             params, gs = po.pp_param_list(model[j], out["grads"][j])
             po.sgd_step(params, gs, lr)
-    worst = {"loss": max(abs(a - b) / abs(b) for a, b in zip(losses, ref)), "grad": 0.0, "update": 0.0}
-    for jj, j in enumerate(eng.local):
+    worst = {"loss": max(abs(a - b) / abs(b) for a, b in zip(losses, ref)), "grad": 0.0, "update": 0.0,
+             "loss_1gpu": max(abs(a - b) / abs(b) for a, b in zip(losses, losses1)), "grad_1gpu": 0.0,
+             "update_1gpu": 0.0}
+    for j in local_ranks:
         for l in range(L):
-            g, want = grads[jj][l], ref_grads[j][l]
-            for nm in ("local", "compressor", "bias"):
-                worst["grad"] = max(worst["grad"], nerr(g[nm], want[nm]))
-            for i, d in g["decompressors"].items():
-                worst["grad"] = max(worst["grad"], nerr(d, want["decompressors"][i]))
-            v = eng.layer_views(jj, l)
-            for nm in ("local", "compressor", "bias"):
-                worst["update"] = max(worst["update"], nerr(v[nm].double().cpu().numpy() - model0[j][l][nm],
-                                                            model[j][l][nm] - model0[j][l][nm]))
-            for i, d in v["decompressors"].items():
-                w0, w1 = model0[j][l]["decompressors"][i], model[j][l]["decompressors"][i]
-                worst["update"] = max(worst["update"], nerr(d.double().cpu().numpy() - w0, w1 - w0))
-    w = torch.tensor([worst["loss"], worst["grad"], worst["update"]], device="cuda", dtype=torch.float64)
+            want_g = dict(tensors({**ref_grads[j][l]}))
+            w0 = dict(tensors(model0[j][l]))
+            w1 = dict(tensors(model[j][l]))
+            g1 = dict(tensors(grads1[(j, l)]))
+            u1 = dict(tensors(weights1[(j, l)]))
+            for nm, g in tensors(grads[(j, l)]):
+                worst["grad"] = max(worst["grad"], nerr(g, want_g[nm]))
+                worst["grad_1gpu"] = max(worst["grad_1gpu"], nerr(g, g1[nm]))
+            for nm, wt in tensors(weights[(j, l)]):
+                worst["update"] = max(worst["update"], nerr(wt - w0[nm], w1[nm] - w0[nm]))
+                worst["update_1gpu"] = max(worst["update_1gpu"], nerr(wt - w0[nm], u1[nm] - w0[nm]))
+    keys = list(worst)
+    w = torch.tensor([worst[k_] for k_ in keys], device="cuda", dtype=torch.float64)
     dist.all_reduce(w, op=dist.ReduceOp.MAX)
-    ok = w[0] <= tol_l and w[1] <= tol_g and w[2] <= tol_u
+    worst = dict(zip(keys, (float(v) for v in w)))
+    tol = {"loss": tol_l, "grad": tol_g, "update": tol_u, "loss_1gpu": tol_e, "grad_1gpu": tol_e, "update_1gpu": tol_e}
+    ok = all(worst[k_] <= tol[k_] for k_ in keys)
     if rank == 0:
         print(json.dumps({"world": world, "dtype": args.dtype, "graph": args.graph, "p": p, "losses": losses,
-                          "oracle": ref, "worst": {"loss": float(w[0]), "grad": float(w[1]), "update": float(w[2])},
-                          "tol": {"loss": tol_l, "grad": tol_g, "update": tol_u}, "fused": bool(eng.fused),
-                          "nvrs": bool(eng.nvrs), "bwd_fused": bool(eng.bwd_fused), "pass": bool(ok)}), flush=True)
+                          "oracle": ref, "one_gpu": losses1, "worst": worst, "tol": tol, **plan, "pass": bool(ok)}),
+              flush=True)
     torch.cuda.synchronize()
-    dist.barrier()
-    eng.close()
     dist.barrier()
     dist.destroy_process_group()
     sys.stdout.flush()
