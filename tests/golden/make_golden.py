@@ -10,6 +10,7 @@ reference tree is not there); it only reads the committed .npz files.
 from __future__ import annotations
 
 import os
+import zlib
 import sys
 
 import numpy as np
@@ -148,7 +149,7 @@ def main():
                             ("g_bias", g.bias), ("delta", res[r].deltas[l]),
                             ("received", res[r].tape[l].phantom_grad),
                             ("preact", res[r].tape[l].preact)):
-                idx = _sample_idx(w.size, hash((r, l, name)) % 10000)
+                idx = _sample_idx(w.size, zlib.crc32(f"{r}:{l}:{name}".encode()) % 10000)
                 c1[q + name + "_idx"] = idx
                 c1[q + name + "_val"] = w.ravel()[idx]
                 c1[q + name + "_norm"] = np.array(np.linalg.norm(w))

