@@ -277,6 +277,16 @@ typedef struct {
 } ppx_wgrad_item;
 ppx_status ppx_wgrad(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad_item* items, void* stream);
 
+/* phantom.py:199-207 + 239-267 in ONE LPT-scheduled launch of the 2-SM kernel (bf16): the error
+   compression of the n local ranks io[] (as ppx_error_phantoms_n, into contrib [p][B, ldk]; with
+   sc the peer-owned slots are also stored into their owner's staging area over NVLink and counted,
+   as ppx_error_phantoms_scatter; with accumulate the slots add to contrib instead) scheduled
+   FIRST on every cluster, followed by the weight-gradient requests items[] (as ppx_wgrad).  The
+   engine uses it when a GPU owns one or two logical ranks: the reduce-scatter then overlaps the
+   weight gradients, and the recurrence (ppx_backward_delta_n) follows ppx_reduce_received. */
+ppx_status ppx_backward_wgrad_errors(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad_item* items,
+                                     int32_t n, const ppx_rank_io* io, int32_t B, void* contrib,
+                                     const ppx_scatter* sc, int32_t accumulate, void* stream);
 /* phantom.py:210-267 as one launch: the weight gradients (+ fused update) of `nitems` items and the
    error recurrence of the n ranks (io as for ppx_backward_delta_n), tiles scheduled longest-first
    over the clusters.  The layer's reduced phantom gradient must already be in place. */

@@ -118,6 +118,8 @@ _SIGS = {
                                   _vp, _i64, _vp, _i64, _fp, _vp]),
     "ppx_colsum": (_i32, [_vp, _i32, _i32, _i32, _vp, _i64, _fp, _i32, _vp]),
     "ppx_optimizer_step": (_i32, [_vp, _i32, _fp, _fp, _fp, _fp, _fp, _i64, _i32, _vp, _vp, _vp]),
+    "ppx_backward_wgrad_errors": (_i32, [_vp, _i32, _i32, ctypes.POINTER(WgradItem), _i32, ctypes.POINTER(RankIO), _i32,
+                                          _vp, ctypes.POINTER(Scatter), _i32, _vp]),
     "ppx_hyper_advance": (_i32, [_vp, _vp, _vp, ctypes.c_double, ctypes.c_double, _vp]),
     "ppx_gemm": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _i64, _i32, _vp, _i64,
                         _i32, ctypes.POINTER(Epilogue), _vp]),

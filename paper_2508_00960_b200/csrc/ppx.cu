@@ -409,6 +409,7 @@ struct Builder {
   };
   std::vector<PendingSeg> pend[ppx::MAX_PROBS];
   bool prob_bmn[ppx::MAX_PROBS] = {};
+  int prio[ppx::MAX_PROBS] = {};   // LPT schedule: higher priority tiles are scheduled first
 
   static int pick_bn(int nb_extent, int gran) {
     int ntiles = (int)cdiv(nb_extent, ppx::BN_MAX);
@@ -425,6 +426,7 @@ struct Builder {
     memset(pr, 0, sizeof(*pr));
     pend[idx].clear();
     prob_bmn[idx] = b_mn;
+    prio[idx] = 0;
     pr->M = M;
     pr->nb_extent = nb_extent;
     pr->nblk = nblk;
@@ -549,6 +551,7 @@ struct Builder {
     tail.npb = (int)cdiv(tail.nb_extent, half);
     pend[ti] = pend[li];
     prob_bmn[ti] = prob_bmn[li];
+    prio[ti] = prio[li];
   }
 
   static void dbg_pending(const char* where) {
@@ -644,13 +647,15 @@ struct Builder {
       // least-loaded cluster; every role of a cluster walks the same list
       const int sms_avail = ctx->num_sms - ctx->reserved_sms;
       const int C = tiles < sms_avail / 2 ? tiles : sms_avail / 2;
-      std::vector<std::pair<double, int>> cost(tiles);
+      // priority problems (prio[i] > 0, e.g. error compression whose outputs other GPUs wait
+      // for) are placed first, so they head every cluster's list
+      std::vector<std::tuple<int, double, int>> cost(tiles);
       for (int i = 0; i < P.nprobs; ++i) {
         const Problem& pr = P.probs[i];
         int kst = 0;
         for (int g = 0; g < pr.nsegs; ++g) kst += pr.segs[g].k_tiles;
         const double c = (kst + 4.0) * pr.BN / 256.0;
-        for (int t = pr.tile_begin; t < pr.tile_begin + ptiles(pr); ++t) cost[t] = {-c, t};
+        for (int t = pr.tile_begin; t < pr.tile_begin + ptiles(pr); ++t) cost[t] = {-prio[i], -c, t};
       }
       std::stable_sort(cost.begin(), cost.end());
       std::vector<double> load(C, 0.0);
@@ -659,8 +664,8 @@ struct Builder {
         int best = 0;
         for (int c = 1; c < C; ++c)
           if (load[c] < load[best]) best = c;
-        load[best] -= ct.first;
-        lists[best].push_back(ct.second);
+        load[best] -= std::get<1>(ct);
+        lists[best].push_back(std::get<2>(ct));
       }
       int o = 0;
       for (int c = 0; c < C; ++c) {
@@ -1446,6 +1451,90 @@ ppx_status ppx_backward_fused(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const 
     if (st != PPX_OK) return st;
   }
   b.lpt = getenv("PPX_NO_LPT") == nullptr;
+  ppx_status st = b.launch();
+  if (st != PPX_OK) return st;
+  for (int i = 0; i < nitems; ++i) {
+    st = wgrad_bias(ctx, dt, items[i], (cudaStream_t)stream);
+    if (st != PPX_OK) return st;
+  }
+  return PPX_OK;
+}
+
+// Error-compression problems (phantom.py:199-205) of the n local ranks io[] into `contrib` ([p]
+// slots of [B, ldk]): one K-concatenated problem per slot i that has a contributor (segment j reads
+// D_{i->j}); peer-owned slots are also copied to their owner's staging area over NVLink with the
+// owner's arrival counter bumped (sc, as ppx_error_phantoms_scatter), or the slots accumulate
+// into what `contrib` holds (accumulate: one GPU running its logical ranks one launch at a time).
+static ppx_status add_error_problems(ppx_ctx* ctx, ppx_dtype dt, Builder& b, int32_t n, const ppx_rank_io* io,
+                                     int32_t B, void* contrib, const ppx_scatter* sc, int accumulate, int prio) {
+  const int p = io[0].layer->p, s = io[0].layer->s, k = io[0].layer->k;
+  Flat f(s, k, p);
+  const int es = dt == PPX_FP32 ? 4 : 2;
+  const int64_t slot_bytes = (int64_t)B * f.ldk * es;
+  const int kt = (int)cdiv(s, b.BK);
+  for (int i = 0; i < p; ++i) {
+    int nseg = 0;
+    for (int j = 0; j < n; ++j) nseg += io[j].layer->rank != i;
+    if (!nseg) continue;
+    Problem* pr = b.new_problem(B, k, 1, true);
+    if (!pr) return b.status;
+    b.prio[pr - b.P.probs] = prio;
+    for (int j = 0; j < n; ++j) {
+      const ppx_layer* L = io[j].layer;
+      if (L->rank == i) continue;
+      Opnd a{view2(io[j].x, B, s, io[j].ld_x)};
+      Opnd d{view3(elem(dt, L->w, f.dec), p - 1, s, k, f.ldk, (int64_t)s * f.ldk)};
+      d.mn = 1;
+      d.slot_base = i - (i > L->rank ? 1 : 0);
+      b.add_segment(pr, a, d, kt, kt);
+    }
+    char* local = (char*)contrib + (int64_t)i * slot_bytes;
+    pr->epi.out = t2(local, f.ldk, dt == PPX_FP32);
+    if (accumulate) pr->epi.flags |= ppx::EP_ACCUM;
+    if (sc) {
+      const int g = i / n;
+      if (g != sc->rank) {
+        char* dst = (char*)sc->stage[g] + ((int64_t)sc->rank * n + (i - g * n)) * slot_bytes;
+        pr->epi.nrep = 1;
+        pr->epi.rep_off[0] = (long long)(dst - local);
+        pr->epi.narrive = 1;
+        pr->epi.arrive_units = 1;
+        pr->epi.arrive[0] = sc->arrive[g];
+      }
+    }
+  }
+  return b.ok() ? PPX_OK : b.status;
+}
+
+// Error compression of layer l + the weight gradients that do not need r_l as ONE LPT-scheduled
+// launch, the error-compression tiles first (their outputs are what the reduce-scatter moves, so
+// with sc the NVLink scatter overlaps the weight-gradient tiles); the recurrence follows after
+// the received error phantoms are reduced (ppx_reduce_received / the caller's reduce-scatter).
+ppx_status ppx_backward_wgrad_errors(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad_item* items,
+                                     int32_t n, const ppx_rank_io* io, int32_t B, void* contrib,
+                                     const ppx_scatter* sc, int32_t accumulate, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (nitems < 0 || (nitems > 0 && !items) || n < 1 || !io || B < 1 || !contrib || dt != PPX_BF16 ||
+      n > ppx::MAX_SEGS || (sc && (accumulate || !sc->stage || !sc->arrive || sc->rank < 0 || sc->rank >= sc->world)))
+    return fail(ctx, PPX_E_CONFIG, "ppx_backward_wgrad_errors: bad arguments");
+  const int p = io[0].layer->p, s = io[0].layer->s, k = io[0].layer->k;
+  for (int j = 0; j < n; ++j) {
+    const ppx_layer* L = io[j].layer;
+    if (bad_layer(L) || !io[j].x || L->s != s || L->k != k || L->p != p || (j && L->rank <= io[j - 1].layer->rank))
+      return fail(ctx, PPX_E_CONFIG, "ppx_backward_wgrad_errors: ranks must share (s, k, p) and ascend");
+  }
+  if (sc && (p % sc->world || p / sc->world != n))
+    return fail(ctx, PPX_E_CONFIG, "ppx_backward_wgrad_errors: scatter needs all p / world local ranks");
+  Builder b(ctx, dt, stream);
+  if (p > 1) {
+    ppx_status st = add_error_problems(ctx, dt, b, n, io, B, contrib, sc, accumulate, 1);
+    if (st != PPX_OK) return st;
+  }
+  for (int i = 0; i < nitems; ++i) {
+    ppx_status st = wgrad_add(ctx, dt, b, items[i]);
+    if (st != PPX_OK) return st;
+  }
+  b.lpt = true;
   ppx_status st = b.launch();
   if (st != PPX_OK) return st;
   for (int i = 0; i < nitems; ++i) {

@@ -55,7 +55,8 @@ class PhantomEngine:
                  optimizer: str = "sgd", lr: float = 1e-4, betas=(0.9, 0.999), eps: float = 1e-8,
                  dtype: torch.dtype = torch.bfloat16, seed: int = 0, ctx: _lib.Context | None = None,
                  fused: bool | None = None, nvrs: bool | None = None, group: int | None = None,
-                 bwd_fused: bool | None = None, store_output: bool = False, capture: bool = False):
+                 bwd_fused: bool | None = None, k3_fused: bool | None = None, store_output: bool = False,
+                 capture: bool = False):
         """Launch-plan switches (None = the default plan; every plan computes the same step):
 
         fused      compression + phantom all-gather + forward of a layer as ONE launch (bf16, s and k
@@ -65,8 +66,12 @@ class PhantomEngine:
                    error-compression epilogue instead of NCCL; default when a GPU owns >= 2 ranks.
         group      logical ranks per grouped launch (default all R; 1 = the per-GPU launch shapes of
                    a run with one logical rank per GPU, on one GPU).
+        k3_fused   error compression + weight gradients of a layer as one LPT-scheduled launch
+                   (error tiles first), then the recurrence once r_l is in: the NVLink
+                   reduce-scatter runs under the weight gradients.  Default when a launch holds
+                   one logical rank (world > 1 with nvrs and <= 2 ranks per GPU, or group=1).
         bwd_fused  weight gradients + error recurrence of a layer as one LPT-scheduled launch per
-                   group; default when each launch holds one logical rank.
+                   group (the plan before k3_fused; used when k3_fused is off).
         store_output  keep the output layer's y (training steps never read it back).
         capture    keep the raw weight gradients (fp32, flat layout) and every layer's delta of the
                    last eager step (parity tests; CUDA-graph replays do not refresh the deltas).
@@ -137,7 +142,7 @@ class PhantomEngine:
         nvrs_ok = world > 1 and dtype == torch.bfloat16 and R <= 8 and k % 8 == 0
         if nvrs and not nvrs_ok:
             raise ConfigurationError("NVLink reduce-scatter needs world > 1, bf16, <= 8 ranks per GPU and k % 8 == 0")
-        self.nvrs = (nvrs_ok and R >= 2) if nvrs is None else bool(nvrs)
+        self.nvrs = nvrs_ok if nvrs is None else bool(nvrs)
         # IPC-shared phantom / staging region (world > 1): needed by the fused forward's in-kernel
         # all-gather and by the NVLink reduce-scatter
         self.p2p = world > 1 and (self.fused or self.nvrs)
@@ -176,6 +181,15 @@ class PhantomEngine:
         if bwd_fused and (dtype != torch.bfloat16 or self.group > 3):
             raise ConfigurationError("fused backward needs bf16 and <= 3 logical ranks per launch group")
         self.bwd_fused = auto_bf if bwd_fused is None else bool(bwd_fused)
+        # error compression + weight gradients in one launch (<= 16 problems: p slots + 3 per rank)
+        k3_ok = (dtype == torch.bfloat16 and p > 1 and p + 3 * self.group <= 16 and
+                 ((world > 1 and self.nvrs and self.group == R) or (world == 1 and self.group < R)))
+        if k3_fused and not k3_ok:
+            raise ConfigurationError("fused error compression + weight gradients needs bf16, p + 3 ranks per launch "
+                                     "<= 16 and either the NVLink reduce-scatter or one GPU with per-group launches")
+        self.k3_fused = (k3_ok and self.group <= 2) if k3_fused is None else bool(k3_fused)
+        if self.k3_fused:
+            self.bwd_fused = False
         self._keep = []   # ctypes structs of the launch being built
         self._launches = 0
         self.launch_count = 0
@@ -369,7 +383,8 @@ class PhantomEngine:
     _KERNEL_CALLS = {"ppx_compress", "ppx_forward_update", "ppx_forward_output", "ppx_error_phantoms", "ppx_wgrad",
                      "ppx_backward_delta", "ppx_optimizer_step", "ppx_compress_n", "ppx_forward_n",
                      "ppx_error_phantoms_n", "ppx_forward_fused", "ppx_error_phantoms_scatter", "ppx_reduce_received",
-                     "ppx_backward_fused", "ppx_backward_delta_n", "ppx_hyper_advance"}
+                     "ppx_backward_fused", "ppx_backward_delta_n", "ppx_hyper_advance",
+                     "ppx_backward_wgrad_errors"}
 
     def _call(self, name, *args, flops=0):
         """ctx.call that counts the launches of our own kernels (NCCL / memsets excluded); under
@@ -486,7 +501,9 @@ class PhantomEngine:
             if self.capture_grads:
                 self.deltas[l] = [self.D[jj][cur].clone() for jj in range(R)]
             ios = [self._io(jj, l, par, x=self.D[jj][cur].data_ptr(), ld_x=s) for jj in range(R)]
-            if nvrs:
+            if self.k3_fused:
+                pass                      # error compression runs inside the weight-gradient launch
+            elif nvrs:
                 # NVLink reduce-scatter: the error-compression epilogue copies every peer-owned
                 # slot into its owner's staging area; reduced after the weight gradients
                 self._call("ppx_error_phantoms_scatter", pdt, R, self._ios(ios), B, self.H[l].data_ptr(),
@@ -502,7 +519,7 @@ class PhantomEngine:
                 for jj in range(R):
                     self._call("ppx_error_phantoms", pdt, ctypes.byref(self._layer(jj, l, par)), B,
                                self.D[jj][cur].data_ptr(), s, self.H[l].data_ptr(), 1, st, flops=self._f_error)
-            if self.world > 1 and not nvrs:
+            if self.world > 1 and not nvrs and not self.k3_fused:
                 self._join(S, self.comm_stream)
                 self._call("ppx_reduce_scatter_to", pdt, self.H[l].data_ptr(), self.Hr[l].data_ptr(), slot, R,
                            self.comm_stream.cuda_stream)
@@ -529,6 +546,28 @@ class PhantomEngine:
                                own, self.Hr[l].data_ptr(), self._pbase + self._rcoff + 4 * l,
                                self._rsepoch[l:].data_ptr(), self.bad.data_ptr(), st)
 
+            if self.k3_fused:
+                # error compression + weight gradients as ONE launch per group (error tiles first;
+                # with nvrs their epilogue stores peer-owned slots into the owners' staging areas,
+                # so the exchange runs under the weight gradients), then r_l, then the recurrence
+                if self.world == 1:
+                    self._call("ppx_zero", self.H[l].data_ptr(), self.H[l].numel() * esz, st)
+                for c0, c1 in self._chunks():
+                    flat = [it for chunk in per_rank[c0:c1] for it in chunk]
+                    arr = (_lib.WgradItem * len(flat))(*flat)
+                    self._keep.append(arr)
+                    sc = ctypes.byref(self._sc[l][0]) if self.world > 1 else None
+                    self._call("ppx_backward_wgrad_errors", pdt, len(flat), arr, c1 - c0, self._ios(ios[c0:c1]), B,
+                               self.H[l].data_ptr(), sc, int(self.world == 1), st,
+                               flops=sum(self._f_item(it) for it in flat) + (c1 - c0) * self._f_error)
+                reduce_received()
+                if l > 0:
+                    rios = [self._recurrence_io(jj, l, par, cur) for jj in range(R)]
+                    for c0, c1 in self._chunks():
+                        self._call("ppx_backward_delta_n", pdt, c1 - c0, self._ios(rios[c0:c1]), B, self.act.code, st,
+                                   flops=(c1 - c0) * self._f_recurrence)
+                    cur = 1 - cur
+                continue
             if self.bwd_fused:
                 # r_l first (exposed), then weight gradients + recurrence of each group as ONE
                 # LPT-scheduled launch

@@ -172,15 +172,18 @@ def test_engine_pair_kernel_matches_oracle(graph):
     _check_updates(eng, model0, model, 1e-1)
 
 
+@pytest.mark.parametrize("k3", [False, True])
 @pytest.mark.parametrize("p", [2, 4])
 @pytest.mark.parametrize("graph", [False, True])
-def test_engine_backward_fused_matches_oracle(graph, p):
-    """bwd_fused=True (group=1): weight gradients (+ fused SGD) and the error recurrence of each layer as ONE
-    launch with a static longest-first tile schedule — bf16 steps against the float64 oracle."""
+def test_engine_backward_fused_matches_oracle(graph, p, k3):
+    """group=1 (one logical rank per launch): k3=False — weight gradients (+ fused SGD) and the error
+    recurrence of each layer as ONE launch with a static longest-first tile schedule; k3=True —
+    error compression + weight gradients as one such launch (error tiles first), then the
+    recurrence — bf16 steps against the float64 oracle."""
     n, k, L, B, lr = 128 * p, 64, 3, 256, 3e-3
-    eng, model, x, y = _setup(n, p, k, L, B, torch.bfloat16, "sgd", lr, group=1)
+    eng, model, x, y = _setup(n, p, k, L, B, torch.bfloat16, "sgd", lr, group=1, k3_fused=k3)
     model0 = copy.deepcopy(model)
-    assert eng.bwd_fused
+    assert (eng.k3_fused, eng.bwd_fused) == (k3, not k3)
     if graph:
         eng.capture()
     losses = []

@@ -30,17 +30,19 @@ def _run(nproc, tool, *args):
 def test_two_gpus_nccl_exchange(dtype, p):
     """Unfused plan: compression, NCCL all-gather, forward; NCCL reduce-scatter.  p = 4: two
     logical ranks per GPU; p = 2: one per GPU."""
-    _run(2, "mp_parity.py", "--dtype", dtype, "--p", p, "--fused", "0", "--nvrs", "0")
+    _run(2, "mp_parity.py", "--dtype", dtype, "--p", p, "--fused", "0", "--nvrs", "0", "--k3", "0")
 
 
-@pytest.mark.parametrize("nvrs", ["1", "0"])
+@pytest.mark.parametrize("nvrs,k3", [("1", "1"), ("1", "0"), ("0", "0")])
 @pytest.mark.parametrize("p", [2, 4])
-def test_two_gpus_fused_forward(p, nvrs):
+def test_two_gpus_fused_forward(p, nvrs, k3):
     """Fused forward over 2 GPUs: the compression tiles store into the peer's phantom buffer over
     NVLink and bump both GPUs' arrival counters; forward tiles wait in-kernel (bf16, k = 64).
     nvrs=1: the reduce-scatter through NVLink too (error-compression epilogue -> owner staging ->
-    in-kernel wait and ascending-rank sum); nvrs=0: NCCL reduce-scatter."""
-    out = _run(2, "mp_parity.py", "--dtype", "bf16", "--p", p, "--k", 64, "--B", 256, "--fused", "1", "--nvrs", nvrs)
+    in-kernel wait and ascending-rank sum), with k3=1 the error compression inside the
+    weight-gradient launch (the default plan); nvrs=0: NCCL reduce-scatter."""
+    out = _run(2, "mp_parity.py", "--dtype", "bf16", "--p", p, "--k", 64, "--B", 256, "--fused", "1", "--nvrs", nvrs,
+               "--k3", k3)
     assert '"fused": true' in out
 
 

@@ -70,7 +70,8 @@ def _step_and_check(eng, ts, steps=2, sensitivity=True):
 @pytest.mark.parametrize("n,p,k,L,B,kw", [
     (512, 4, 32, 3, 64, {}),            # 1-SM kernel (k not a multiple of 64), grouped launches
     (1024, 2, 16, 4, 64, {}),           # C1 shapes in bf16
-    (512, 4, 64, 3, 256, {"group": 1}),  # per-rank launches + fused backward, small
+    (512, 4, 64, 3, 256, {"group": 1}),  # per-rank launches, [error compression + wgrad] fused, small
+    (512, 4, 64, 3, 256, {"group": 1, "k3_fused": False}),  # per-rank, [wgrad + recurrence] fused
     (768, 4, 24, 2, 96, {"fused": False}),   # ragged k / batch tiles
 ])
 def test_small_shapes_teacher_forced(n, p, k, L, B, kw):
@@ -89,9 +90,13 @@ def test_c3_grouped_default_plan():
     eng.close()
 
 
-def test_c3_one_rank_per_launch():
-    eng, ts = _engine(16384, 8, 128, 8, 8192, group=1)
-    assert eng.group == 1 and eng.bwd_fused and not eng.fused
+@pytest.mark.parametrize("plan", ["k3_fused", "bwd_fused"])
+def test_c3_one_rank_per_launch(plan):
+    """k3_fused (default): [error compression + weight gradients] LPT launch per rank, then the
+    recurrence; bwd_fused: error compression, then [weight gradients + recurrence] per rank."""
+    eng, ts = _engine(16384, 8, 128, 8, 8192, group=1, k3_fused=plan == "k3_fused")
+    assert eng.group == 1 and not eng.fused
+    assert (eng.k3_fused, eng.bwd_fused) == ((True, False) if plan == "k3_fused" else (False, True))
     _step_and_check(eng, ts)
     eng.close()
 

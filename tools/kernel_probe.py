@@ -2,9 +2,10 @@
 
     python tools/kernel_probe.py KIND [--group 1|8] [--iters 20] [--config c3] [--ncu]
 
-KIND: forward (fused / grouped forward of layer 3), error (error compression of layer 3),
-wgrad (grouped weight gradients of layer 3), bwd (fused weight-gradient + recurrence launch of
-layer 3 with group=1), recurrence, compress.  The launches are issued exactly as
+KIND: forward (fused / grouped forward), error (error compression), wgrad (grouped weight
+gradients), bwd (fused weight-gradient + recurrence launch, group=1 --k3 0), wgrad_errors (fused
+error-compression + weight-gradient launch, group=1), recurrence, compress — the middle launch of
+that kind in the step (--index to pick another).  The launches are issued exactly as
 PhantomEngine._step_body issues them (the engine records every kernel call of an eager step with
 its ABI arguments; the probe re-issues the chosen one) back to back behind a ~0.1 s device spin
 (so host launch cost never starves the GPU) and timed with CUDA events.  --ncu brackets ONE eager launch with cudaProfilerStart/Stop (run under
@@ -20,6 +21,7 @@ from paper_2508_00960_b200.engine import PhantomEngine
 
 KINDS = {"forward": ("ppx_forward_fused", "ppx_forward_n"), "error": ("ppx_error_phantoms_n", "ppx_error_phantoms",
          "ppx_error_phantoms_scatter"), "wgrad": ("ppx_wgrad",), "bwd": ("ppx_backward_fused",),
+         "wgrad_errors": ("ppx_backward_wgrad_errors",),
          "recurrence": ("ppx_backward_delta_n",), "compress": ("ppx_compress_n",)}
 
 ap = argparse.ArgumentParser()
@@ -29,9 +31,11 @@ ap.add_argument("--config", default="c3")
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--index", type=int, default=-1, help="which matching launch of the step (default: middle)")
 ap.add_argument("--ncu", action="store_true")
+ap.add_argument("--k3", default="auto", help="k3_fused plan: auto|0|1")
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
-eng = PhantomEngine(cfg["n"], cfg["p"], cfg["k"], cfg["layers"], cfg["batch"], lr=3e-6, group=args.group or None)
+eng = PhantomEngine(cfg["n"], cfg["p"], cfg["k"], cfg["layers"], cfg["batch"], lr=3e-6, group=args.group or None,
+                    k3_fused=None if args.k3 == "auto" else args.k3 == "1")
 xs, ts = bench.make_data(eng, 1, cfg)
 for par in (0, 1):
     eng.set_batch(xs, ts, par)

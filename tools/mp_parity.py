@@ -88,6 +88,7 @@ def main():
     ap.add_argument("--lr", type=float, default=3e-3)
     ap.add_argument("--fused", default="auto")
     ap.add_argument("--nvrs", default="auto")
+    ap.add_argument("--k3", default="auto", help="fused error compression + weight gradients")
     ap.add_argument("--layers", type=int, default=3)
     ap.add_argument("--infer", type=int, default=0, help="forward_only calls back to back instead of training")
     args = ap.parse_args()
@@ -112,12 +113,13 @@ def main():
     x = rng.standard_normal((n, B))
     y = np.maximum(rng.standard_normal((n, B)), 0.0)
     eng = PhantomEngine(n, p, k, L, B, world=world, rank=rank, device=local, uid=uid[0], lr=lr, dtype=dtype,
-                        fused=tri(args.fused), nvrs=tri(args.nvrs), capture=True)
+                        fused=tri(args.fused), nvrs=tri(args.nvrs), k3_fused=tri(args.k3), capture=True)
     if args.infer:
         eng.load_params(model)
         return infer(args, eng, model, x, rank, world, s, p, L, tol_l)
     losses, grads, weights = run_engine(eng, model, x, y, args)
-    plan = {"fused": bool(eng.fused), "nvrs": bool(eng.nvrs), "bwd_fused": bool(eng.bwd_fused)}
+    plan = {"fused": bool(eng.fused), "nvrs": bool(eng.nvrs), "bwd_fused": bool(eng.bwd_fused),
+            "k3_fused": bool(eng.k3_fused)}
     local_ranks = list(eng.local)
     torch.cuda.synchronize()
     dist.barrier()
@@ -176,6 +178,8 @@ def infer(args, eng, model, x, rank, world, s, p, L, tol):
     stream order and compared with the oracle's pp_forward.  With L = 1 nothing but the engine's
     inference fence orders call i+1's NVLink phantom stores after the peers' reads of call i."""
     x2 = -0.5 * x
+    eng.set_batch([torch.from_numpy(x[j * s:(j + 1) * s].T.copy()).cuda() for j in eng.local],
+                  [torch.zeros((eng.B, s), device="cuda") for _ in eng.local], 0)
     eng.set_batch([torch.from_numpy(x2[j * s:(j + 1) * s].T.copy()).cuda() for j in eng.local],
                   [torch.zeros((eng.B, s), device="cuda") for _ in eng.local], 1)
     outs = []

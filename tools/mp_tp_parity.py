@@ -63,7 +63,8 @@ def main():
     losses = []
     eng.step(graph=False)
     losses.append(eng.read_loss())
-    eng.capture()
+    if args.steps > 1:
+        eng.capture()
     for _ in range(args.steps - 1):
         eng.step()
         losses.append(eng.read_loss())
