@@ -263,7 +263,7 @@ def make_data(eng, seed, cfg):
     g.manual_seed(seed)
     X = torch.randn((B, n), generator=g, device=eng.dev).to(torch.bfloat16)
     Xr = torch.empty_like(X)
-    eng.ctx.call("ppx_bias_act", eng.pdt, B, n, X.data_ptr(), n, None, 0, Xr.data_ptr(), n,
+    eng.ctx.call("ppx_bias_act", 0, B, n, X.data_ptr(), n, None, 0, Xr.data_ptr(), n,
                  torch.cuda.current_stream().cuda_stream)
     xs, ts = [], []
     for jj, j in enumerate(eng.local):
@@ -271,8 +271,8 @@ def make_data(eng, seed, cfg):
         gt.manual_seed(seed * 7919 + j)
         W = (torch.randn((s, n), generator=gt, device=eng.dev) / n ** 0.5).to(torch.bfloat16)
         T = kernels.gemm(Xr, W, transpose_b=True, out_dtype=torch.bfloat16, relu=True, ctx=eng.ctx)
-        xs.append(X[:, j * s:(j + 1) * s].contiguous())
-        ts.append(T)
+        xs.append(X[:, j * s:(j + 1) * s].to(eng.dtype).contiguous())
+        ts.append(T.to(eng.dtype))
         del W
     del X, Xr
     return xs, ts
@@ -397,7 +397,11 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--optimizer", default="sgd", choices=["sgd", "adam"])
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"],
+                    help="fp32 = the 3xTF32 parity tier (throughput reported separately from the bf16 headline)")
     ap.add_argument("--energy-seconds", type=float, default=20.0)
+    ap.add_argument("--k3", default="auto", choices=["auto", "0", "1"],
+                    help="A/B of the backward launch plan (k3_fused); default = the engine's choice")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -432,11 +436,14 @@ def main():
     if args.config == "c5":
         return run_inference_sweep(args, cfg, D, uid, peak)
 
+    dtype = torch.float32 if args.dtype == "fp32" else torch.bfloat16
     eng = PhantomEngine(n, p, k, L, B, world=world, rank=rank, device=local_rank, uid=uid,
-                        optimizer=args.optimizer, lr=3e-6, dtype=torch.bfloat16)
+                        optimizer=args.optimizer, lr=3e-6, dtype=dtype,
+                        k3_fused=None if args.k3 == "auto" else args.k3 == "1")
     xs, ts = make_data(eng, 1234, cfg)
     eng.set_batch(xs, ts, 0)
     eng.set_batch(xs, ts, 1)
+    plan = {"fused": eng.fused, "nvrs": eng.nvrs, "k3": eng.k3_fused, "bwd": eng.bwd_fused, "group": eng.group}
 
     # warm-up: eager step (sets kernel attributes), capture, graph replays
     eng.step(graph=False)
@@ -471,10 +478,14 @@ def main():
                 "kernel_sum_frac_of_burst": step_flops / (kern_ms / 1e3) / 1e12 / peak,
                 "flops_tagged_per_step": flops_check, "flops_algorithmic_per_step": step_flops,
                 "kernels": kernels}
+    if args.dtype == "fp32":
+        roofline["tier_note"] = ("3xTF32 tier: three kind::tf32 MMAs per product at half the bf16 rate, so its "
+                                 "tensor ceiling is 1/6 of the bf16 peak (frac_of_tier_ceiling = 6 x frac)")
+        roofline["frac_of_tier_ceiling"] = 6 * roofline["frac"]
 
     # ---- inference (config C5 at this k): forward-only graph replays of the same model
     inference = None
-    if args.config in ("c3", "c2"):
+    if args.config in ("c3", "c2") and args.dtype == "bf16":
         inference = time_inference(eng, D, args.steps, use_graph, peak)
 
     # ---- NVML energy over >= energy_seconds of steady-state training steps
@@ -484,7 +495,7 @@ def main():
     e2e = None if args.no_e2e else time_e2e(eng, D, xs, ts, args.steps, use_graph, B)
 
     r1 = None
-    if world == 1 and p > 1 and not args.no_r1 and args.config in ("c3", "c2"):
+    if world == 1 and p > 1 and not args.no_r1 and args.config in ("c3", "c2") and args.dtype == "bf16":
         eng.close()
         del eng
         torch.cuda.empty_cache()
@@ -496,7 +507,7 @@ def main():
         cpu = cpu_baseline(args, cfg)
 
     tp = None
-    if not args.no_tp and L % 2 == 0 and args.config != "c4":
+    if not args.no_tp and L % 2 == 0 and args.config != "c4" and args.dtype == "bf16":
         tp = run_tp(args, cfg, D, eng, uid)
     elif eng is not None:
         D.barrier()
@@ -506,14 +517,16 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": f"phantom FFN {args.config}: n={n}, L={L}, p={p} logical ranks, k={k}, "
                                    f"batch {B}, ReLU, mean loss, {args.optimizer.upper()}; "
                                    f"{p // world} logical rank(s) per GPU",
                        "global_batch": B, "width": n, "layers": L, "p": p, "k": k,
                        "parallelism": f"phantom pp{p} over {world} GPU(s)",
                        "l2": "working set per step (weights + activations) exceeds the 126 MB L2; no flush",
-                       "graphs": use_graph},
+                       "graphs": use_graph,
+                       "plan": {"fused_forward": bool(plan["fused"]), "nvlink_reduce_scatter": bool(plan["nvrs"]),
+                                "k3_fused": bool(plan["k3"]), "bwd_fused": bool(plan["bwd"]), "group": plan["group"]}},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -32,6 +32,7 @@ ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--index", type=int, default=-1, help="which matching launch of the step (default: middle)")
 ap.add_argument("--ncu", action="store_true")
 ap.add_argument("--k3", default="auto", help="k3_fused plan: auto|0|1")
+ap.add_argument("--noaccum", action="store_true", help="ppx_error_phantoms: overwrite instead of accumulate")
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
 eng = PhantomEngine(cfg["n"], cfg["p"], cfg["k"], cfg["layers"], cfg["batch"], lr=3e-6, group=args.group or None,
@@ -65,6 +66,8 @@ idx = len(match) // 2 if args.index < 0 else args.index
 name, cargs = match[idx]
 same = [c for c in match[:idx] if c[0] == name]          # ordinal of the pick among its ABI call
 flops = [fl for nm, ms, fl in seq if nm == name][len(same)]
+if args.noaccum and name == "ppx_error_phantoms":
+    cargs = cargs[:6] + (0,) + cargs[7:]
 keep = eng._keep            # the ctypes structs the recorded arguments point into
 eng._keep = []              # never cleared again: the replays below reuse them
 

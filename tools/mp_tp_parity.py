@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--layers", type=int, default=4)
     ap.add_argument("--B", type=int, default=64)
     ap.add_argument("--lr", type=float, default=3e-3)
+    ap.add_argument("--graph", type=int, default=1)
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -63,10 +64,10 @@ def main():
     losses = []
     eng.step(graph=False)
     losses.append(eng.read_loss())
-    if args.steps > 1:
+    if args.steps > 1 and args.graph:
         eng.capture()
     for _ in range(args.steps - 1):
-        eng.step()
+        eng.step(graph=bool(args.graph))
         losses.append(eng.read_loss())
     Wd = [w.copy() for w in W]
     bd = [v.copy() for v in b]
