@@ -191,3 +191,55 @@ def check_engine_step(eng, par, bias0, targets, loss, act="relu"):
                 if p > 1:
                     share["backward"] = min(share["backward"], rel(Re @ Ws[j]["compressor"], D[j] @ Ws[j]["local"]))
     return worst, share
+
+
+def train_sgd_curve(model, x, y, layers, batch, lr, epochs, dtype, reduction="mean", act="relu"):
+    """The reference's PP training loop (training.py:276-309: contiguous mini-batches, pre-update
+    iteration loss, epoch loss = mean of iteration losses, SGD) restated with this module's
+    per-layer functions in `dtype` on the CPU — used to measure how far exact fp32 arithmetic
+    drifts from float64 over a training run.  model: oracle-format (list over ranks of lists over
+    layers of numpy dicts), x / y: (n, samples) numpy."""
+    p = len(model)
+    n = x.shape[0]
+    s = n // p
+    t = lambda a: torch.tensor(a, dtype=dtype)   # noqa: E731  (a copy: updates stay local)
+    W = [[{"local": t(lay["local"]), "compressor": t(lay["compressor"]),
+           "dec": torch.stack([t(lay["decompressors"][i]) for i in _peers(p, j)]), "bias": t(lay["bias"])}
+          for lay in model[j]] for j in range(p)]
+    X = [t(x[j * s:(j + 1) * s].T) for j in range(p)]
+    Y = [t(y[j * s:(j + 1) * s].T) for j in range(p)]
+    iters = x.shape[1] // batch
+    hist = []
+    for _ in range(epochs):
+        losses = []
+        for it in range(iters):
+            sl = slice(it * batch, (it + 1) * batch)
+            acts = [[X[j][sl] for j in range(p)]]
+            Gs = []
+            for l in range(layers):
+                G = [compress(W[j][l], acts[-1][j]) for j in range(p)]
+                Gs.append(G)
+                acts.append([forward_layer(W[j][l], j, acts[-1][j], G, act)[1] for j in range(p)])
+            loss, D = 0.0, []
+            for j in range(p):
+                out = acts[-1][j]
+                lj, d = loss_and_delta(out, out, Y[j][sl], reduction, act)   # ReLU mask: out > 0 == pre > 0
+                loss += lj
+                D.append(d)
+            losses.append(loss)
+            grads = [[None] * layers for _ in range(p)]
+            for l in range(layers - 1, -1, -1):
+                R = error_phantoms([W[j][l] for j in range(p)], D)
+                for j in range(p):
+                    grads[j][l] = param_grads(j, D[j], acts[l][j], Gs[l], R[j])
+                if l > 0:
+                    D = [backward_delta(W[j][l], D[j], R[j], acts[l][j], act) for j in range(p)]
+            for j in range(p):
+                for l in range(layers):
+                    g, w = grads[j][l], W[j][l]
+                    w["local"] -= lr * g["local"]
+                    w["compressor"] -= lr * g["compressor"]
+                    w["dec"] -= lr * g["dec"]
+                    w["bias"] -= lr * g["bias"]
+        hist.append(sum(losses) / len(losses))
+    return hist

@@ -65,3 +65,31 @@ def test_teacher_matches_oracle(n, p, k, L, B):
                 d_prev = tc.backward_delta(Ws[j], D[j], R[j], Y[j])
                 assert tc.nerr(d_prev, _t(ref["deltas"][j][l - 1])) < tol
     assert abs(total - ref["global_loss"]) <= tol * abs(ref["global_loss"])
+
+
+def test_fp32_arithmetic_drift_on_c1_training():
+    """Why the fp32 tier's C1 training curves are held to 5e-3 per epoch (tests/
+    test_train_engine_gpu.py), not 1e-4: the same training loop in EXACT fp32 arithmetic on the
+    CPU (this restatement, no tensor cores) already drifts from float64 by more than 1e-4 by the
+    second epoch — the reference problem amplifies rounding — while staying inside 5e-3.  The
+    float64 run itself reproduces the reference's golden curve (tests/golden/c1.npz)."""
+    import os
+    from paper_2508_00960_b200.phantom import _reference_init_arrays
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "c1.npz"))
+    n, p, k, L, B, seed = (int(v) for v in gold["cfg"])
+    s = n // p
+    model = []
+    for j in range(p):
+        row = []
+        for l in range(L):
+            loc, comp, decs = _reference_init_arrays(n, p, k, L, seed, j, l)
+            row.append({"local": loc, "compressor": comp, "decompressors": decs, "bias": np.zeros(s)})
+        model.append(row)
+    x, y, _ = po.gen_dataset(n, 1024, seed)
+    h64 = tc.train_sgd_curve(model, x, y, L, B, 1e-4, 3, torch.float64)
+    h32 = tc.train_sgd_curve(model, x, y, L, B, 1e-4, 3, torch.float32)
+    np.testing.assert_allclose(h64, gold["train_sgd_hist"], rtol=1e-10)
+    drift = [abs(a - b) / b for a, b in zip(h32, h64)]
+    print("fp32 vs fp64 epoch drift:", drift)
+    assert max(drift) > 1e-4          # 1e-4 per epoch is out of reach of fp32 arithmetic itself
+    assert max(drift) < 5e-3
