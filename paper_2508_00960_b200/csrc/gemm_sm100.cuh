@@ -631,7 +631,9 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
     rows_valid = rows_valid < 0 ? 0 : (rows_valid > 32 ? 32 : rows_valid);
     const int row = row0 + lane;
     const bool row_ok = lane < rows_valid;
-    const uint32_t flags = E.flags;
+    // debug A/B only (PPX_DEBUG_EPI, wrong results): bit 2 drops the ReLU'-mask read, bit 3 the
+    // column sums
+    const uint32_t flags = E.flags & ~((P.dbg & 4) ? EP_MASK : 0u) & ~((P.dbg & 8) ? EP_COLSUM : 0u);
     const bool upd = (flags & (EP_SGD | EP_ADAM)) != 0;
     // per-row input streamed one chunk ahead: target | fp32 master | ReLU mask | accumulated output
     const Tensor2* sa = (flags & EP_LOSS) ? &E.target

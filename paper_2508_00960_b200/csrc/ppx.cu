@@ -686,7 +686,11 @@ struct Builder {
       P.done = ctx->fuse_done;
       P.bad = fuse_bad;
     }
-    P.dbg = (getenv("PPX_DEBUG_NOEPI") ? 1 : 0) | (getenv("PPX_DEBUG_NOWAIT") ? 2 : 0);
+    {
+      const char* ep = getenv("PPX_DEBUG_EPI");
+      P.dbg = (getenv("PPX_DEBUG_NOEPI") ? 1 : 0) | (getenv("PPX_DEBUG_NOWAIT") ? 2 : 0) |
+              (ep && strstr(ep, "mask") ? 4 : 0) | (ep && strstr(ep, "colsum") ? 8 : 0);
+    }
     if (tiles == 0) return PPX_OK;
     cudaError_t e;
     const int sms = ctx->num_sms - ctx->reserved_sms;

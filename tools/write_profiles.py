@@ -1,58 +1,91 @@
-"""Summarise the round-end GPU evidence (gpurun_out/final_*) into profiles/ (tracked)."""
-import csv, io, json, os, subprocess, sys
+"""Summarise this round's GPU evidence (gpurun_out/ev_*, mg_*) into profiles/ (tracked):
+
+  profiles/r2_bench_*.json       the bench lines (1 GPU, 2 / 4 GPUs, C2 / C4 / C5)
+  profiles/r2_launches_*.txt     ncu launch-list share tables of one eager C3 step (grouped N=1 and
+                                 one logical rank per launch), paired with the engine's ABI trace
+  profiles/r2_ncu_*.csv          selected ncu --set full metrics of each launch kind (step shapes)
+  profiles/traffic.json          DRAM bytes per launch of each kind, stamped with the commit
+  profiles/r2_summary.md         the tables quoted in DESIGN.md
+
+    python tools/write_profiles.py [commit]
+"""
+import csv, glob, io, json, os, subprocess, sys
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G, P = os.path.join(ROOT, "gpurun_out"), os.path.join(ROOT, "profiles")
+COMMIT = sys.argv[1] if len(sys.argv) > 1 else subprocess.run(["git", "rev-parse", "--short", "HEAD"], cwd=ROOT,
+                                                              capture_output=True, text=True).stdout.strip()
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "gpc__cycles_elapsed.avg.per_second",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "launch__grid_size", "launch__cluster_dim_x", "sm__cycles_active.avg"]
+CALL_OF = {"forward": "ppx_forward_fused", "wgrad": "ppx_wgrad", "recurrence": "ppx_backward_delta_n",
+           "error": "ppx_error_phantoms_n", "forward__group_1": "ppx_forward_n",
+           "wgrad_errors__group_1": "ppx_backward_wgrad_errors", "recurrence__group_1": "ppx_backward_delta_n (R=1)",
+           "bwd__group_1__k3_0": "ppx_backward_fused"}
 
 
-def ncu_raw(rep, keys):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(out)))
+def raw_metrics(path):
+    rows = list(csv.reader(io.StringIO(open(path).read())))
+    if len(rows) < 3:
+        return {}
     hdr, units, vals = rows[0], rows[1], rows[2]
-    return {h: (v, u) for h, u, v in zip(hdr, units, vals) if h in keys}
+    return {h: (v, u) for h, u, v in zip(hdr, units, vals) if h in KEYS}
 
 
-def step_table(launches, trace, label):
-    return subprocess.run([sys.executable, os.path.join(ROOT, "tools", "step_profile.py"), launches, trace, label],
-                          capture_output=True, text=True).stdout
+def to_bytes(v, u):
+    x = float(v.replace(",", ""))
+    return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
 
 
-keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "gpc__cycles_elapsed.avg.per_second",
-        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
-        "lts__t_bytes.sum", "launch__grid_size", "launch__cluster_dim_x"]
-k1 = ncu_raw(os.path.join(G, "final_k1.ncu-rep"), keys)
-rd = float(k1["dram__bytes_read.sum"][0]) * (1e6 if k1["dram__bytes_read.sum"][1] == "Mbyte" else 1e9 if k1["dram__bytes_read.sum"][1] == "Gbyte" else 1)
-wr = float(k1["dram__bytes_write.sum"][0]) * (1e6 if k1["dram__bytes_write.sum"][1] == "Mbyte" else 1e9 if k1["dram__bytes_write.sum"][1] == "Gbyte" else 1)
-json.dump({"kernel": "gemm_pair_kernel as ppx_forward_update (C3 layer, one logical rank: M=8192, N=2048, K=2048+7*128)",
-           "source": "ncu --set full --clock-control none (tools/final_profile.sh, k1_probe.py launch 3), dram__bytes_read.sum + dram__bytes_write.sum",
-           "dram_bytes_per_launch": int(rd + wr), "algorithmic_bytes_per_launch": 52690944,
-           "note": "algorithmic = Y 32 MiB + gathered phantoms 14 MiB + L 8 MiB + D 3.5 MiB read, Y_out 32 MiB written; "
-                   "DRAM write < 32 MiB because the output stays L2-resident at kernel end"},
-          open(os.path.join(P, "k1_traffic.json"), "w"), indent=1)
-lines = ["# Round 1 (final) — B200 evidence", "",
-         "Commands: `tools/final_profile.sh` on one GPU (ncu only after the same command exited 0 without it);",
-         "multi-GPU lines from `bench.py` under torchrun on one 4-GPU box. Per-launch ncu times are serialised",
-         "and cold-cache at uncapped clocks: compare shares, not absolutes.", "",
-         "## K1 (fused forward GEMM, the roofline kernel) — ncu --set full", "", "| metric | value |", "|---|---|"]
-for kk in keys:
-    if kk in k1:
-        lines.append(f"| {kk} | {k1[kk][0]} {k1[kk][1]} |")
-lines += ["", "## One C3 training step on 1 GPU (8 logical ranks, grouped launches)", "", "```",
-          step_table(os.path.join(G, "final_launches.csv"), os.path.join(G, "final_trace.json"), "N=1 grouped (R=8)").strip(),
-          "```", "", "## The same step with one logical rank per launch (per-GPU kernels of an 8-GPU run; unfused forward)", "",
-          "```", step_table(os.path.join(G, "final_launches_r1.csv"), os.path.join(G, "final_trace_r1.json"),
-                             "R=1 shapes").strip(), "```", "", "## bench.py lines", ""]
-for f in ["final_bench_n1.json", "final_bench_ref.json", "final_bench_n2.json", "final_bench_n4.json", "final_bench_c2_n4.json"]:
-    path = os.path.join(G, f)
-    if os.path.exists(path) and os.path.getsize(path):
-        d = json.loads(open(path).read().strip().splitlines()[-1])
-        keep = {k: d.get(k) for k in ("impl", "value", "ms_per_step", "n_gpus", "e2e", "roofline", "clocks", "cpu_baseline",
-                                       "pp_vs_tp", "energy", "comm_bytes_per_step_per_gpu") if k in d}
-        if d.get("tp"):
-            keep["tp"] = {k: d["tp"].get(k) for k in ("value", "ms_per_step", "comm_bytes_per_step_per_gpu", "j_per_epoch")}
-        lines += [f"### {f}", "", "```json", json.dumps(keep, indent=1), "```", ""]
-        os.makedirs(P, exist_ok=True)
-        open(os.path.join(P, "r1_" + f), "w").write(open(path).read())
-open(os.path.join(P, "r1_final_summary.md"), "w").write("\n".join(lines) + "\n")
-for src, dst in [("final_launches.csv", "r1_final_launches_n1.csv"), ("final_launches_r1.csv", "r1_final_launches_r1shapes.csv")]:
-    open(os.path.join(P, dst), "w").write(open(os.path.join(G, src)).read())
-print("\n".join(lines))
+def main():
+    os.makedirs(P, exist_ok=True)
+    md = [f"# Round 2 — B200 evidence (commit {COMMIT})", ""]
+    for src in sorted(glob.glob(os.path.join(G, "ev_bench.json")) + glob.glob(os.path.join(G, "mg_*.json"))):
+        try:
+            line = json.loads(open(src).read().strip().splitlines()[-1])
+        except Exception:
+            continue
+        name = os.path.basename(src).replace("ev_bench", "c3_n1").replace("mg_", "")
+        json.dump(line, open(os.path.join(P, f"r2_bench_{name}"), "w"), indent=1)
+        md.append(f"* `r2_bench_{name}`: value {line.get('value')} {line.get('unit')}, "
+                  f"ms/step {line.get('ms_per_step')}, clocks {line.get('clocks', {}).get('sm_mhz')} MHz")
+    md.append("")
+    for g in ("8", "1"):
+        lst, tr = os.path.join(G, f"ev_launches_g{g}.csv"), os.path.join(G, f"ev_trace_g{g}.json")
+        if os.path.exists(lst) and os.path.exists(tr):
+            out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_step_table.py"), lst, tr,
+                                  f"C3 eager step, group={g}"], capture_output=True, text=True).stdout
+            open(os.path.join(P, f"r2_launches_g{g}.txt"), "w").write(out)
+            md += ["```", out.rstrip(), "```", ""]
+    traffic = {}
+    md += ["| launch (step shapes) | ncu us | SM MHz | tensor pipe % active | DRAM MB / launch |", "|---|---|---|---|---|"]
+    for path in sorted(glob.glob(os.path.join(G, "ev_full_*.raw.csv"))):
+        tag = os.path.basename(path)[len("ev_full_"):-len(".raw.csv")]
+        m = raw_metrics(path)
+        if not m:
+            continue
+        with open(os.path.join(P, f"r2_ncu_{tag}.csv"), "w") as f:
+            w = csv.writer(f)
+            w.writerow(["metric", "value", "unit"])
+            for k in KEYS:
+                if k in m:
+                    w.writerow([k, m[k][0], m[k][1]])
+        dram = to_bytes(*m["dram__bytes_read.sum"]) + to_bytes(*m["dram__bytes_write.sum"])
+        call = CALL_OF.get(tag, tag)
+        shape = "R=1 (one logical rank per launch)" if "group_1" in tag else "R=8 (grouped, N=1)"
+        traffic.setdefault(call, {"dram_bytes_per_launch": dram, "commit": COMMIT, "shape": f"C3, {shape}"})
+        md.append(f"| {call} ({shape}) | {m['gpu__time_duration.sum'][0]} | "
+                  f"{float(m['gpc__cycles_elapsed.avg.per_second'][0]) * (1000 if m['gpc__cycles_elapsed.avg.per_second'][1] == 'Ghz' else 1):.0f} | "
+                  f"{m['sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active'][0]} | {dram / 1e6:.1f} |")
+    json.dump(traffic, open(os.path.join(P, "traffic.json"), "w"), indent=1)
+    for f in ("epi_ab.txt", "tp_probe.txt", "sanitize_summary.txt", "mgpu_ab.jsonl"):
+        if os.path.exists(os.path.join(G, f)):
+            md += ["", f"## {f}", "```", open(os.path.join(G, f)).read().rstrip(), "```"]
+    open(os.path.join(P, "r2_summary.md"), "w").write("\n".join(md) + "\n")
+    print("\n".join(md))
+
+
+if __name__ == "__main__":
+    main()
