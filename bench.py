@@ -443,7 +443,8 @@ def main():
     xs, ts = make_data(eng, 1234, cfg)
     eng.set_batch(xs, ts, 0)
     eng.set_batch(xs, ts, 1)
-    plan = {"fused": eng.fused, "nvrs": eng.nvrs, "k3": eng.k3_fused, "bwd": eng.bwd_fused, "group": eng.group}
+    plan = {"fused": eng.fused, "nvrs": eng.nvrs, "k3": eng.k3_fused, "bwd": eng.bwd_fused, "group": eng.group,
+            "bits": eng.mask_bits}
 
     # warm-up: eager step (sets kernel attributes), capture, graph replays
     eng.step(graph=False)
@@ -526,7 +527,8 @@ def main():
                        "l2": "working set per step (weights + activations) exceeds the 126 MB L2; no flush",
                        "graphs": use_graph,
                        "plan": {"fused_forward": bool(plan["fused"]), "nvlink_reduce_scatter": bool(plan["nvrs"]),
-                                "k3_fused": bool(plan["k3"]), "bwd_fused": bool(plan["bwd"]), "group": plan["group"]}},
+                                "k3_fused": bool(plan["k3"]), "bwd_fused": bool(plan["bwd"]), "group": plan["group"],
+                                "mask_bits": bool(plan["bits"])}},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -152,6 +152,11 @@ typedef struct {
   const void* mask;    int64_t ld_m;    /* backward: ReLU' source (pre_prev or y_prev) */
   const void* received;                 /* backward: [B, ldk] reduced phantom gradient */
   float* colsum;                        /* output layer / backward: += batch sums of the delta */
+  void* bits;          int64_t ld_bits; /* optional, bf16 2-SM launches, s % 32 == 0: forward — also
+                                           store ReLU'(pre) as a bit mask (bit i of uint32 word
+                                           [row, col / 32] = y > 0, ld_bits words per row);
+                                           backward — read the ReLU' mask from such bits instead of
+                                           `mask` (1/16 of the bytes) */
 } ppx_rank_io;
 
 /* n x ppx_compress in one launch */

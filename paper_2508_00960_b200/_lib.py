@@ -62,7 +62,7 @@ class RankIO(ctypes.Structure):
     """ppx_rank_io: one logical rank's operands in a grouped launch."""
     _fields_ = [("layer", ctypes.POINTER(Layer)), ("x", _vp), ("ld_x", _i64), ("out", _vp), ("ld_out", _i64),
                 ("aux", _vp), ("ld_aux", _i64), ("target", _vp), ("ld_t", _i64), ("mask", _vp), ("ld_m", _i64),
-                ("received", _vp), ("colsum", _vp)]
+                ("received", _vp), ("colsum", _vp), ("bits", _vp), ("ld_bits", _i64)]
 
 
 GRAD_LOCAL, GRAD_COMP, GRAD_DEC, GRAD_BIAS, GRAD_ALL = 1, 2, 4, 8, 15

@@ -73,6 +73,9 @@ enum : uint32_t {
   EP_ADAM = 1u << 8,      // Adam on master with m, v moments ; out = cast(master)
   EP_GRAD = 1u << 9,      // also store the raw gradient to `aux` (fp32)
   EP_FINITE = 1u << 10,   // flag non-finite accumulator values
+  EP_BITS = 1u << 11,     // also store the ReLU'(pre) bit mask, bit i of word (row, col/32) = v > 0, to
+                          // `preact` as uint32 words (ld in words; forward layers feeding a recurrence)
+  EP_MASKBITS = 1u << 12, // EP_MASK from such a bit mask in `mask` instead of the bf16 layer output
 };
 
 struct Operand {
@@ -638,7 +641,7 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
     // per-row input streamed one chunk ahead: target | fp32 master | ReLU mask | accumulated output
     const Tensor2* sa = (flags & EP_LOSS) ? &E.target
                         : upd            ? &E.master
-                        : (flags & EP_MASK) ? &E.mask
+                        : ((flags & EP_MASK) && !(flags & EP_MASKBITS)) ? &E.mask
                         : (flags & EP_ACCUM) ? &E.out : nullptr;
     const long long a_ss = sa && (upd || sa == &E.out) ? sa->slot_stride : 0;
     const long long a_rb = sa ? (long long)row * sa->ld : 0;
@@ -666,6 +669,20 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
           const long long mo = (long long)os * E.master.slot_stride + m_rb + col0;
           prefetch_row(E.adam_m, mo, n);
           prefetch_row(E.adam_v, mo, n);
+        }
+      }
+    }
+    // bit-mask words of this warp's chunks (c = grp, grp + 2, ...), loaded before the wait
+    uint32_t mbits[BN_MAX / 64];
+    if (flags & EP_MASKBITS) {
+#pragma unroll
+      for (int u = 0; u < BN_MAX / 64; ++u) {
+        const int c = grp + 2 * u;
+        mbits[u] = 0u;
+        if (c < nchunks && row_ok) {
+          int col0, nv, os;
+          geom(c, col0, nv, os);
+          if (nv > 0) mbits[u] = __ldg(reinterpret_cast<const uint32_t*>(E.mask.ptr) + row * E.mask.ld + (col0 >> 5));
         }
       }
     }
@@ -747,16 +764,20 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
             if (E.out.ptr) store32(E.out, ooff, nvalid, v);
             store32(E.aux, (long long)row * E.aux.ld + col0, nvalid, tg);
           }
-          if (flags & EP_COLSUM) {
+          if (flags & EP_COLSUM) {   // bias gradient: one global reduction per column and warp
             const float cs = warp_transpose_sum(tg, lane);
-            if (lane < nvalid) atomicAdd(cs_smem + as * BN_MAX + c * 32 + lane, cs);
+            if (lane < nvalid) atomicAdd(E.colsum + col0 + lane, cs);
           }
         } else {
           if (flags & EP_RELU) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
           }
-          if (flags & EP_MASK) {
+          if (flags & EP_MASKBITS) {
+            const uint32_t mw = mbits[(c - grp) >> 1];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = (ok(i) && ((mw >> i) & 1u)) ? v[i] : 0.f;
+          } else if (flags & EP_MASK) {
             float mk[32];
             pre_finish(E.mask, a_row + col0, nvalid, live, pa, mk);
 #pragma unroll
@@ -770,13 +791,19 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
             for (int i = 0; i < 32; ++i) v[i] += (ok(i) && live) ? o[i] : 0.f;
           }
           if (live) store32(E.out, ooff, nvalid, v);
+          if ((flags & EP_BITS) && live) {   // ReLU'(pre) = (y > 0) for the recurrence, 1 bit each
+            uint32_t w = 0u;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) w |= (ok(i) && v[i] > 0.f) ? (1u << i) : 0u;
+            reinterpret_cast<uint32_t*>(E.preact.ptr)[row * E.preact.ld + (col0 >> 5)] = w;
+          }
           if (flags & EP_COLSUM) {
             if (!F) {
 #pragma unroll
               for (int i = 0; i < 32; ++i) v[i] = ok(i) ? v[i] : 0.f;
             }
             const float cs = warp_transpose_sum(v, lane);
-            if (lane < nvalid) atomicAdd(cs_smem + as * BN_MAX + c * 32 + lane, cs);
+            if (lane < nvalid) atomicAdd(E.colsum + col0 + lane, cs);
           }
         }
       };
@@ -792,19 +819,6 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
       if (lane == 0) atomicAdd(E.loss, loss_acc * E.loss_scale);
     }
     if ((flags & EP_FINITE) && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(E.bad, 1);
-    if ((flags & EP_COLSUM) && nchunks) {
-      // the epilogue warps' column sums meet in shared memory; one warp (rotating) flushes the
-      // tile's sums with one global atomic per column and clears its buffer (reused two tiles on,
-      // after the next tile's barrier)
-      asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
-      if (warp == (iter & (NUM_EPI_WARPS - 1))) {
-        float* cb = cs_smem + as * BN_MAX;
-        for (int j = lane; j < pr.BN; j += 32) {
-          if (j < ncols) atomicAdd(E.colsum + tc.nin + j, cb[j]);
-          cb[j] = 0.f;
-        }
-      }
-    }
     // hand the stored tile to the publisher warps (a full barrier: it also waits until they took
     // the previous published tile, so barrier generations never mix)
     if (publishes(E)) asm volatile("bar.sync 4, %0;" ::"n"(NUM_EPI_WARPS * 32 + 64) : "memory");

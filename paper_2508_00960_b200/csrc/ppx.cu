@@ -631,6 +631,9 @@ struct Builder {
       }
     }
     if (use_pair && !lpt && !getenv("PPX_NO_TAILSPLIT")) split_tail(ctx->num_sms / 2 - ctx->reserved_sms / 2);
+    for (int i = 0; i < P.nprobs; ++i)
+      if ((P.probs[i].epi.flags & (ppx::EP_BITS | ppx::EP_MASKBITS)) && (P.probs[i].BN % 32 || P.probs[i].nspan > 1))
+        return fail(ctx, PPX_E_CONFIG, "bit-mask epilogues need 32-aligned, non-spanning tiles");
     for (int i = 0; i < P.nprobs && ok(); ++i)
       for (const PendingSeg& ps : pend[i]) finalize(&P.probs[i], ps);
     if (!ok()) return status;
@@ -920,9 +923,16 @@ static ppx_status add_forward(ppx_ctx* ctx, ppx_dtype dt, Builder& b, const ppx_
   pr->epi.flags = ppx::EP_BIAS | (act == PPX_RELU ? ppx::EP_RELU : 0u);
   pr->epi.out = t2(io.out, io.ld_out, f32);
   if (!output_layer) {
+    if (io.aux && io.bits) return fail(ctx, PPX_E_CONFIG, "forward: pre-activation and bit mask are exclusive");
     if (io.aux) {
       pr->epi.flags |= ppx::EP_PREACT;
       pr->epi.preact = t2(io.aux, io.ld_aux, f32);
+    }
+    if (io.bits) {   // the recurrence's ReLU' mask, 1 bit per element (the preact slot carries it)
+      if (f32 || L->s % 32 || act != PPX_RELU || io.ld_bits < L->s / 32)
+        return fail(ctx, PPX_E_CONFIG, "forward: bit masks need bf16, ReLU and s % 32 == 0");
+      pr->epi.flags |= ppx::EP_BITS;
+      pr->epi.preact = t2(io.bits, io.ld_bits, 0);
     }
   } else {
     pr->epi.flags |= ppx::EP_LOSS | (io.colsum ? ppx::EP_COLSUM : 0u);
@@ -1395,7 +1405,7 @@ ppx_status ppx_wgrad(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad
 static ppx_status add_backward(ppx_ctx* ctx, ppx_dtype dt, Builder& b, const ppx_rank_io& io, int32_t B,
                                ppx_act act_prev) {
   const ppx_layer* L = io.layer;
-  if (bad_layer(L) || B < 1 || !io.x || !io.out || (act_prev == PPX_RELU && !io.mask))
+  if (bad_layer(L) || B < 1 || !io.x || !io.out || (act_prev == PPX_RELU && !io.mask && !io.bits))
     return fail(ctx, PPX_E_CONFIG, "backward_delta: bad arguments");
   if (L->p > 1 && !io.received) return fail(ctx, PPX_E_SEQUENCING, "backward_delta: received gradient missing");
   Flat f(L->s, L->k, L->p);
@@ -1413,7 +1423,12 @@ static ppx_status add_backward(ppx_ctx* ctx, ppx_dtype dt, Builder& b, const ppx
   if (!pr) return b.status;
   const int f32 = dt == PPX_FP32;
   pr->epi.out = t2(io.out, io.ld_out, f32);
-  if (act_prev == PPX_RELU) {
+  if (act_prev == PPX_RELU && io.bits) {
+    if (f32 || L->s % 32 || io.ld_bits < L->s / 32)
+      return fail(ctx, PPX_E_CONFIG, "backward_delta: bit masks need bf16 and s % 32 == 0");
+    pr->epi.flags |= ppx::EP_MASK | ppx::EP_MASKBITS;
+    pr->epi.mask = t2(io.bits, io.ld_bits, 0);
+  } else if (act_prev == PPX_RELU) {
     pr->epi.flags |= ppx::EP_MASK;
     pr->epi.mask = t2(const_cast<void*>(io.mask), io.ld_m, f32);
   }

@@ -56,7 +56,7 @@ class PhantomEngine:
                  dtype: torch.dtype = torch.bfloat16, seed: int = 0, ctx: _lib.Context | None = None,
                  fused: bool | None = None, nvrs: bool | None = None, group: int | None = None,
                  bwd_fused: bool | None = None, k3_fused: bool | None = None, store_output: bool = False,
-                 capture: bool = False):
+                 capture: bool = False, mask_bits: bool | None = None):
         """Launch-plan switches (None = the default plan; every plan computes the same step):
 
         fused      compression + phantom all-gather + forward of a layer as ONE launch (bf16, s and k
@@ -73,6 +73,9 @@ class PhantomEngine:
         bwd_fused  weight gradients + error recurrence of a layer as one LPT-scheduled launch per
                    group (the plan before k3_fused; used when k3_fused is off).
         store_output  keep the output layer's y (training steps never read it back).
+        mask_bits  the forward epilogue also stores ReLU'(pre) of every inner layer as a bit mask
+                   and the recurrence reads it instead of the bf16 activations (1/16 of the mask
+                   bytes); default for bf16 ReLU with s % 64 == 0.
         capture    keep the raw weight gradients (fp32, flat layout) and every layer's delta of the
                    last eager step (parity tests; CUDA-graph replays do not refresh the deltas).
         """
@@ -129,6 +132,13 @@ class PhantomEngine:
                 self.Y[1][jj][l] = self.Y[0][jj][l]
         self.Tgt = [[torch.empty((B, s), dtype=dtype, device=self.dev) for _ in range(R)] for _ in range(2)]
         self.D = [[torch.empty((B, s), dtype=dtype, device=self.dev) for _ in range(2)] for _ in range(R)]
+        bits_ok = dtype == torch.bfloat16 and self.act is Activation.RELU and s % 64 == 0 and layers > 1
+        if mask_bits and not bits_ok:
+            raise ConfigurationError("bit masks need bf16, ReLU and s % 64 == 0")
+        self.mask_bits = bits_ok if mask_bits is None else bool(mask_bits)
+        # bits[jj][l] = ReLU'(pre_{l-1}) = (Y[l] > 0) packed 32 per int32 word, l = 1 .. L-1
+        self.bits = ([[None] + [torch.zeros((B, s // 32), dtype=torch.int32, device=self.dev) for _ in range(1, layers)]
+                      for _ in range(R)] if self.mask_bits else None)
         self.bad = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.group = R if group is None else max(1, min(int(group), R))
         auto_fused = (dtype == torch.bfloat16 and s % 64 == 0 and k % 64 == 0 and R <= 8 and self.group == R)
@@ -436,6 +446,8 @@ class PhantomEngine:
                 if last:   # the output y itself is never read by the backward pass: not stored
                     kw.update(out=None if self.skip_output else kw["out"], aux=self.D[jj][0].data_ptr(), ld_aux=s,
                               target=self.Tgt[par][jj].data_ptr(), ld_t=s, colsum=self.gbias[jj, l].data_ptr())
+                elif train and self.mask_bits:   # the recurrence of layer l+1 masks with these bits
+                    kw.update(bits=self.bits[jj][l + 1].data_ptr(), ld_bits=s // 32)
                 ios.append(self._io(jj, l, par, **kw))
             return ios
 
@@ -486,10 +498,11 @@ class PhantomEngine:
 
     def _recurrence_io(self, jj, l, par, cur):
         """[delta | r].[L ; C] -> delta_{l-1} with the ReLU'-mask and d-bias epilogue."""
+        kw = dict(bits=self.bits[jj][l].data_ptr(), ld_bits=self.s // 32) if self.mask_bits else {}
         return self._io(jj, l, par, x=self.D[jj][cur].data_ptr(), ld_x=self.s, out=self.D[jj][1 - cur].data_ptr(),
                         ld_out=self.s, mask=self.Y[par][jj][l].data_ptr() if self.act is Activation.RELU else None,
                         ld_m=self.s, received=self._received(l, self.local[jj]),
-                        colsum=self.gbias[jj, l - 1].data_ptr())
+                        colsum=self.gbias[jj, l - 1].data_ptr(), **kw)
 
     def _backward(self, par, S):
         st, pdt, B, s, R, L = S.cuda_stream, self.pdt, self.B, self.s, self.R, self.L

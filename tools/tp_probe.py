@@ -81,3 +81,13 @@ for step in range(2):
             D = (Dya @ Wa[m]) * (Xs[m] > 0)
             msg.append(f"D{m - 1 + 1}in {rel(eng2.Dfull[1], D):.1e}")
     print(f"[intermediates] step {step} par {par}: " + "  ".join(msg))
+    Xe, Te = f64(eng2.X[par][L // 2]), f64(eng2.Tgt[par])
+    De = (Xe - Te) * (Xe > 0) / B
+    print(f"   engine-internal: Dout vs (X_P - T) mask / B from the engine's own buffers {rel(eng2.Dfull[0], De):.1e}; "
+          f"Tgt vs y {rel(eng2.Tgt[par], torch.from_numpy(y.T.copy()).cuda().double()):.1e}; "
+          f"loss {float(eng2.loss.item()):.6f} vs {0.5 * float(((Xe - Te) ** 2).sum()) / B:.6f}")
+    Xr = Xs[-1]
+    flips = int(((Xr > 0) != (Xe > 0)).sum())
+    near = float(Xe[(Xr > 0) != (Xe > 0)].abs().max()) if flips else 0.0
+    print(f"   output ReLU mask flips engine vs float64: {flips} of {Xr.numel()} (largest |y| at a flip {near:.2e}); "
+          f"|X_P engine - f64| max {float((Xe - Xr).abs().max()):.2e}")
