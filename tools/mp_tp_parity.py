@@ -11,8 +11,9 @@ row block (column-parallel layers) / column block (row-parallel layers) / biases
 -lr * that gradient.  A ReLU whose pre-activation is within rounding of 0 can take the other
 branch in fp32 than in float64 (one such element moves a gradient by ~1e-2 at this size), so a
 step whose engine activations show such a mask flip against the oracle's forward is held to the
-flip tolerance and reported; all other steps to 1e-4 (fp32 tier) / 3e-2 (bf16).  Losses: 1e-4 /
-2e-2.  Rank 0 prints one JSON verdict.
+flip tolerance (5e-2 fp32; 1.5e-1 bf16, whose bf16 activations flip ~150-250 of the 65k ReLUs
+per step at this size) and reported; all other steps to 1e-4 (fp32 tier) / 3e-2 (bf16).  Losses:
+1e-4 / 2e-2.  Rank 0 prints one JSON verdict.
 """
 import argparse, json, os, sys
 import numpy as np
@@ -61,7 +62,7 @@ def main():
     n, L, B, lr = args.width, args.layers, args.B, args.lr
     f32 = args.dtype == "fp32"
     dtype = torch.float32 if f32 else torch.bfloat16
-    tol_l, tol_u, tol_flip = (1e-4, 1e-4, 5e-2) if f32 else (2e-2, 3e-2, 1e-1)
+    tol_l, tol_u, tol_flip = (1e-4, 1e-4, 5e-2) if f32 else (2e-2, 3e-2, 1.5e-1)
     rng = np.random.default_rng(5)
     a = np.sqrt(6.0 / (2 * n))
     W = [rng.uniform(-a, a, (n, n)) for _ in range(L)]
