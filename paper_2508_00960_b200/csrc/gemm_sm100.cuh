@@ -86,6 +86,7 @@ struct Operand {
                      // 2 = 5D map {atom, 8 rows, atoms, K groups, slots}: canonical interleaved tile
   int slot_base;
   int slot_skip;     // raw slot index >= skip is shifted by one (own rank excluded); INT_MAX = none
+                     // < 0: decompressor-stack mode of rank -skip-1 (see op_slot)
 };
 
 struct Segment {
@@ -563,6 +564,13 @@ __device__ __forceinline__ void end_epoch(const GemmParams& P) {
 
 __device__ __forceinline__ int op_slot(const Operand& o, int kblk, int qn) {
   int raw = o.slot_src == 1 ? kblk : (o.slot_src == 2 ? qn : 0);
+  if (o.slot_skip < 0) {
+    // decompressor stack of rank j = -slot_skip - 1 (sources ascending, j itself absent): the
+    // absolute source slot maps to its stack index, and j's own slot to an index past the end,
+    // which TMA fills with zeros (a slot-pair tile whose one half has no contribution from j)
+    const int src = o.slot_base + raw, j = -o.slot_skip - 1;
+    return src < j ? src : (src == j ? 0x7fff : src - 1);
+  }
   return o.slot_base + raw + (raw >= o.slot_skip ? 1 : 0);
 }
 
@@ -590,23 +598,32 @@ __device__ __forceinline__ void publisher_loop(const GemmParams& P, int t0, int 
     const int rbase = tc.m0 + (int)crank * BM;
     int nrows = pr.M - rbase;
     nrows = nrows < 0 ? 0 : (nrows > BM ? BM : nrows);
-    const int ncols = pr.nb_extent - tc.nin < pr.BN ? pr.nb_extent - tc.nin : pr.BN;
-    if (E.nrep) {
+    // a spanning tile holds two consecutive N blocks (slots); every block it covers is published
+    const int nhalf = pr.nspan > 1 ? 2 : 1;
+    const int ncols = pr.nspan > 1 ? pr.nb_extent
+                                   : (pr.nb_extent - tc.nin < pr.BN ? pr.nb_extent - tc.nin : pr.BN);
+    int cells = 0;
+    for (int h = 0; h < nhalf; ++h) {
+      const int q = tc.qn + h;
+      if (q >= pr.nblk) break;
+      cells += nrows * ncols;
+      if (!E.nrep) continue;
       const int es = E.out.f32 ? 4 : 2;
       const int upr = ncols * es / 16;
       const long long ldb = E.out.ld * es;
-      const char* src = reinterpret_cast<const char*>(E.out.ptr) + (long long)rbase * ldb + (long long)tc.nin * es;
+      const char* src = reinterpret_cast<const char*>(E.out.ptr) + (long long)q * E.out.slot_stride * es +
+                        (long long)rbase * ldb + (long long)tc.nin * es;
       for (int u = tid; u < nrows * upr; u += 64) {
         const int r = u / upr;
         const long long off = r * ldb + (long long)(u - r * upr) * 16;
-        const uint4 q = *reinterpret_cast<const uint4*>(src + off);
-        for (int i = 0; i < E.nrep; ++i) *reinterpret_cast<uint4*>(const_cast<char*>(src) + E.rep_off[i] + off) = q;
+        const uint4 v = *reinterpret_cast<const uint4*>(src + off);
+        for (int i = 0; i < E.nrep; ++i) *reinterpret_cast<uint4*>(const_cast<char*>(src) + E.rep_off[i] + off) = v;
       }
     }
     asm volatile("bar.sync 5, 64;" ::: "memory");
     if (E.narrive && tid == 0) {
       __threadfence_system();
-      const int amount = E.arrive_units ? nrows * ncols / 8 : 1;
+      const int amount = E.arrive_units ? cells / 8 : 1;
       for (int i = 0; i < E.narrive; ++i)
         asm volatile("red.relaxed.sys.global.add.s32 [%0], %1;" ::"l"(E.arrive[i]), "r"(amount) : "memory");
     }

@@ -1061,6 +1061,64 @@ ppx_status ppx_error_phantoms(ppx_ctx* ctx, ppx_dtype dt, const ppx_layer* L, in
   return b.launch();
 }
 
+// One error-compression problem over `nslots` (1 or 2) consecutive output slots i0.. of the
+// [p][B, ldk] contribution buffer: segment j (every local rank contributing to one of the slots)
+// reads rank j's decompressor stack in stack mode, so with two slots each CTA of a pair tile takes
+// one slot and rank j's own slot (absent from its stack) loads as TMA zeros.  Two slots make
+// 256-wide tiles (one 128-wide slot per CTA) instead of L2-bandwidth-bound 128-wide ones.
+// Peer-owned slots are also copied to their owner's staging area (sc) — both slots of a pair
+// belong to the same owner when R is even — or accumulate into `contrib`.
+static Problem* error_slot_problem(Builder& b, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B,
+                                   void* contrib, int i0, int nslots, const ppx_scatter* sc, int accumulate) {
+  const int p = io[0].layer->p, s = io[0].layer->s, k = io[0].layer->k;
+  Flat f(s, k, p);
+  const int es = dt == PPX_FP32 ? 4 : 2;
+  const int64_t slot_bytes = (int64_t)B * f.ldk * es;
+  const int kt = (int)cdiv(s, b.BK);
+  int nseg = 0;
+  for (int j = 0; j < n; ++j) {
+    const int r = io[j].layer->rank;
+    nseg += nslots == 2 ? 1 : (r != i0);
+  }
+  if (!nseg) return nullptr;
+  Problem* pr = b.new_problem(B, k, nslots, true);
+  if (!pr) return nullptr;
+  for (int j = 0; j < n; ++j) {
+    const ppx_layer* L = io[j].layer;
+    if (nslots == 1 && L->rank == i0) continue;
+    Opnd a{view2(io[j].x, B, s, io[j].ld_x)};
+    Opnd d{view3(elem(dt, L->w, f.dec), p - 1, s, k, f.ldk, (int64_t)s * f.ldk)};
+    d.mn = 1;
+    if (nslots == 2) {
+      d.slot_src = 2;
+      d.slot_base = i0;
+      d.slot_skip = -(L->rank + 1);
+    } else {
+      d.slot_base = i0 - (i0 > L->rank ? 1 : 0);
+    }
+    b.add_segment(pr, a, d, kt, kt);
+  }
+  char* local = (char*)contrib + (int64_t)i0 * slot_bytes;
+  pr->epi.out = t2(local, f.ldk, dt == PPX_FP32, (int64_t)B * f.ldk);
+  if (accumulate) pr->epi.flags |= ppx::EP_ACCUM;
+  if (sc) {
+    const int g = i0 / n;
+    if (g != sc->rank) {
+      char* dst = (char*)sc->stage[g] + ((int64_t)sc->rank * n + (i0 - g * n)) * slot_bytes;
+      pr->epi.nrep = 1;
+      pr->epi.rep_off[0] = (long long)(dst - local);
+      pr->epi.narrive = 1;
+      pr->epi.arrive_units = 1;
+      pr->epi.arrive[0] = sc->arrive[g];
+    }
+  }
+  return pr;
+}
+
+// slot pairs need bf16 (2-SM tiles), an even slot count per GPU (a pair never straddles two owners)
+// and k a multiple of 64 (each half one whole 64-atom block per CTA)
+static bool error_pairs(ppx_dtype dt, int n, int p, int k) { return dt == PPX_BF16 && n % 2 == 0 && p % 2 == 0 && k % 64 == 0; }
+
 // Grouped error compression for the n logical ranks one GPU owns (phantom.py:199-205): output
 // slot i = sum over contributing ranks j != i (ascending) of delta_j . D_{i->j}, as ONE
 // K-concatenated problem per slot (segment j reads D_{i->j} = slot i - (i > j) of rank j's
@@ -1092,29 +1150,16 @@ ppx_status ppx_error_phantoms_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx
     }
     return PPX_OK;
   }
+  const int step = error_pairs(dt, n, p, k) ? 2 : 1;
   int i = 0;
   while (i < p) {
     Builder b(ctx, dt, stream);
-    const int kt = (int)cdiv(s, b.BK);
-    for (; i < p && b.P.nprobs < ppx::MAX_PROBS - 1; ++i) {
-      int nseg = 0;
-      for (int j = 0; j < n; ++j) nseg += io[j].layer->rank != i;
-      if (!nseg) continue;
-      Problem* pr = b.new_problem(B, k, 1, true);
-      for (int j = 0; j < n; ++j) {
-        const ppx_layer* L = io[j].layer;
-        if (L->rank == i) continue;
-        Opnd a{view2(io[j].x, B, s, io[j].ld_x)};
-        Opnd d{view3(elem(dt, L->w, f.dec), p - 1, s, k, f.ldk, (int64_t)s * f.ldk)};
-        d.mn = 1;
-        d.slot_base = i - (i > L->rank ? 1 : 0);
-        b.add_segment(pr, a, d, kt, kt);
-      }
-      if (pr) pr->epi.out = t2((char*)contrib + (int64_t)i * B * f.ldk * es, f.ldk, 0);
-    }
+    for (; i < p && b.P.nprobs < ppx::MAX_PROBS - 1; i += step) error_slot_problem(b, dt, n, io, B, contrib, i, step, nullptr, 0);
     ppx_status st = b.launch();
     if (st != PPX_OK) return st;
   }
+  (void)es;
+  (void)f;
   return PPX_OK;
 }
 
@@ -1170,40 +1215,16 @@ ppx_status ppx_error_phantoms_scatter(ppx_ctx* ctx, ppx_dtype dt, int32_t n, con
   Flat f(s, k, p);
   const int R = n, es = 2;
   const int64_t slot_bytes = (int64_t)B * f.ldk * es;
+  const int step = error_pairs(dt, R, p, k) ? 2 : 1;
   int i = 0;
   while (i < p) {
     Builder b(ctx, dt, stream);
-    const int kt = (int)cdiv(s, b.BK);
-    for (; i < p && b.P.nprobs < ppx::MAX_PROBS - 1; ++i) {
-      int nseg = 0;
-      for (int j = 0; j < n; ++j) nseg += io[j].layer->rank != i;
-      if (!nseg) continue;
-      Problem* pr = b.new_problem(B, k, 1, true);
-      for (int j = 0; j < n; ++j) {
-        const ppx_layer* L = io[j].layer;
-        if (L->rank == i) continue;
-        Opnd a{view2(io[j].x, B, s, io[j].ld_x)};
-        Opnd d{view3(elem(dt, L->w, f.dec), p - 1, s, k, f.ldk, (int64_t)s * f.ldk)};
-        d.mn = 1;
-        d.slot_base = i - (i > L->rank ? 1 : 0);
-        b.add_segment(pr, a, d, kt, kt);
-      }
-      if (!pr) break;
-      char* local = (char*)contrib + (int64_t)i * slot_bytes;
-      pr->epi.out = t2(local, f.ldk, 0);
-      const int g = i / R;
-      if (g != sc->rank) {
-        char* dst = (char*)sc->stage[g] + ((int64_t)sc->rank * R + (i - g * R)) * slot_bytes;
-        pr->epi.nrep = 1;
-        pr->epi.rep_off[0] = (long long)(dst - local);
-        pr->epi.narrive = 1;
-        pr->epi.arrive_units = 1;
-        pr->epi.arrive[0] = sc->arrive[g];
-      }
-    }
+    for (; i < p && b.P.nprobs < ppx::MAX_PROBS - 1; i += step) error_slot_problem(b, dt, R, io, B, contrib, i, step, sc, 0);
     ppx_status st = b.launch();
     if (st != PPX_OK) return st;
   }
+  (void)slot_bytes;
+  (void)f;
   return PPX_OK;
 }
 
@@ -1486,43 +1507,15 @@ ppx_status ppx_backward_fused(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const 
 // into what `contrib` holds (accumulate: one GPU running its logical ranks one launch at a time).
 static ppx_status add_error_problems(ppx_ctx* ctx, ppx_dtype dt, Builder& b, int32_t n, const ppx_rank_io* io,
                                      int32_t B, void* contrib, const ppx_scatter* sc, int accumulate, int prio) {
-  const int p = io[0].layer->p, s = io[0].layer->s, k = io[0].layer->k;
-  Flat f(s, k, p);
-  const int es = dt == PPX_FP32 ? 4 : 2;
-  const int64_t slot_bytes = (int64_t)B * f.ldk * es;
-  const int kt = (int)cdiv(s, b.BK);
-  for (int i = 0; i < p; ++i) {
-    int nseg = 0;
-    for (int j = 0; j < n; ++j) nseg += io[j].layer->rank != i;
-    if (!nseg) continue;
-    Problem* pr = b.new_problem(B, k, 1, true);
-    if (!pr) return b.status;
-    b.prio[pr - b.P.probs] = prio;
-    for (int j = 0; j < n; ++j) {
-      const ppx_layer* L = io[j].layer;
-      if (L->rank == i) continue;
-      Opnd a{view2(io[j].x, B, s, io[j].ld_x)};
-      Opnd d{view3(elem(dt, L->w, f.dec), p - 1, s, k, f.ldk, (int64_t)s * f.ldk)};
-      d.mn = 1;
-      d.slot_base = i - (i > L->rank ? 1 : 0);
-      b.add_segment(pr, a, d, kt, kt);
-    }
-    char* local = (char*)contrib + (int64_t)i * slot_bytes;
-    pr->epi.out = t2(local, f.ldk, dt == PPX_FP32);
-    if (accumulate) pr->epi.flags |= ppx::EP_ACCUM;
-    if (sc) {
-      const int g = i / n;
-      if (g != sc->rank) {
-        char* dst = (char*)sc->stage[g] + ((int64_t)sc->rank * n + (i - g * n)) * slot_bytes;
-        pr->epi.nrep = 1;
-        pr->epi.rep_off[0] = (long long)(dst - local);
-        pr->epi.narrive = 1;
-        pr->epi.arrive_units = 1;
-        pr->epi.arrive[0] = sc->arrive[g];
-      }
-    }
+  const int p = io[0].layer->p, k = io[0].layer->k;
+  const int step = error_pairs(dt, n, p, k) ? 2 : 1;
+  for (int i = 0; i < p; i += step) {
+    Problem* pr = error_slot_problem(b, dt, n, io, B, contrib, i, step, sc, accumulate);
+    if (pr) b.prio[pr - b.P.probs] = prio;
+    if (!b.ok()) return b.status;
   }
-  return b.ok() ? PPX_OK : b.status;
+  (void)ctx;
+  return PPX_OK;
 }
 
 // Error compression of layer l + the weight gradients that do not need r_l as ONE LPT-scheduled

@@ -41,11 +41,13 @@ def test_gemm_layouts(dtype, ta, tb, shape):
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
 @pytest.mark.parametrize("s,k,p,R,B", [(256, 128, 8, 8, 512), (256, 128, 8, 3, 256), (128, 32, 4, 4, 64),
-                                       (256, 64, 4, 2, 200), (192, 128, 8, 1, 256)])
+                                       (256, 64, 4, 2, 200), (192, 128, 8, 1, 256), (256, 128, 8, 4, 256),
+                                       (256, 128, 8, 2, 256), (320, 64, 8, 8, 384)])
 def test_error_phantoms_grouped(dtype, s, k, p, R, B):
     """ppx_error_phantoms_n (phantom.py:199-205 for R local ranks in one launch): slot i =
     sum_{j local, j != i} delta_j . D_{i->j}, vs a torch fp32 reference; slots without a
-    contributor keep their previous contents."""
+    contributor keep their previous contents.  Even R with k % 64 == 0 runs slot-pair tiles (one
+    slot per CTA, a rank's own slot loaded as TMA zeros)."""
     import ctypes
     from paper_2508_00960_b200 import _lib, kernels
     from paper_2508_00960_b200.core import flat_offsets

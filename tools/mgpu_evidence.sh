@@ -2,11 +2,13 @@
 # 4-GPU evidence: comm-model fit, C3 bench at N=2 and 4 (TP + e2e + energy), C2 and C4 at N=4,
 # the C5 inference sweep at N=2 and 4, and the 4-GPU parity tests.  Outputs: gpurun_out/mg_*
 mkdir -p gpurun_out
-tr() { python -m torch.distributed.run --nnodes=1 --nproc-per-node $1 --master-addr 127.0.0.1 --master-port $2 "${@:3}"; }
-timeout 900 tr 4 29801 tools/comm_fit.py --out gpurun_out/mg_comm_b200 > gpurun_out/mg_comm.log 2>&1; echo "comm rc=$?"
-timeout 600 tr 2 29802 bench.py --gpus 2 --steps 20 --warmup 5 > gpurun_out/mg_c3_n2.json 2> gpurun_out/mg_c3_n2.err; echo "c3 n2 rc=$?"
-timeout 600 tr 4 29803 bench.py --gpus 4 --steps 20 --warmup 5 > gpurun_out/mg_c3_n4.json 2> gpurun_out/mg_c3_n4.err; echo "c3 n4 rc=$?"
-timeout 600 tr 4 29804 bench.py --gpus 4 --config c2 --steps 20 --warmup 5 --no-tp > gpurun_out/mg_c2_n4.json 2> gpurun_out/mg_c2_n4.err; echo "c2 n4 rc=$?"
-timeout 900 tr 4 29805 bench.py --gpus 4 --config c4 --steps 10 --warmup 3 --no-e2e > gpurun_out/mg_c4_n4.json 2> gpurun_out/mg_c4_n4.err; echo "c4 n4 rc=$?"
-for N in 2 4; do timeout 600 tr $N $((29810+N)) bench.py --gpus $N --config c5 --steps 20 > gpurun_out/mg_c5_n$N.json 2> gpurun_out/mg_c5_n$N.err; echo "c5 n$N rc=$?"; done
+TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
+timeout 900 $TR --nproc-per-node 4 --master-port 29801 tools/comm_fit.py --out gpurun_out/mg_comm_b200 > gpurun_out/mg_comm.log 2>&1; echo "comm rc=$?"
+timeout 600 $TR --nproc-per-node 2 --master-port 29802 bench.py --gpus 2 --steps 20 --warmup 5 > gpurun_out/mg_c3_n2.json 2> gpurun_out/mg_c3_n2.err; echo "c3 n2 rc=$?"
+timeout 600 $TR --nproc-per-node 4 --master-port 29803 bench.py --gpus 4 --steps 20 --warmup 5 > gpurun_out/mg_c3_n4.json 2> gpurun_out/mg_c3_n4.err; echo "c3 n4 rc=$?"
+timeout 600 $TR --nproc-per-node 4 --master-port 29804 bench.py --gpus 4 --config c2 --steps 20 --warmup 5 --no-tp > gpurun_out/mg_c2_n4.json 2> gpurun_out/mg_c2_n4.err; echo "c2 n4 rc=$?"
+timeout 900 $TR --nproc-per-node 4 --master-port 29805 bench.py --gpus 4 --config c4 --steps 10 --warmup 3 --no-e2e > gpurun_out/mg_c4_n4.json 2> gpurun_out/mg_c4_n4.err; echo "c4 n4 rc=$?"
+for N in 2 4; do timeout 600 $TR --nproc-per-node $N --master-port $((29810+N)) bench.py --gpus $N --config c5 --steps 20 > gpurun_out/mg_c5_n$N.json 2> gpurun_out/mg_c5_n$N.err; echo "c5 n$N rc=$?"; done
 timeout 900 python -m pytest tests/test_multigpu_gpu.py -q -rA > gpurun_out/mg_tests.log 2>&1; echo "tests rc=$?"
+for N in 2 4; do timeout 300 $TR --nproc-per-node $N --master-port $((29820+N)) tools/mp_trace.py --config c3 > gpurun_out/mg_trace_c3_n$N.txt 2>&1; echo "trace n$N rc=$?"; done
+timeout 300 $TR --nproc-per-node 4 --master-port 29830 tools/mp_trace.py --config c2 > gpurun_out/mg_trace_c2_n4.txt 2>&1; echo "trace c2 n4 rc=$?"

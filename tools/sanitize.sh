@@ -1,4 +1,6 @@
 #!/bin/bash
+# NOTE: this pool closes compute-sanitizer (runs under it left GPUs needing a reset), so the
+# script is kept for other machines; profiles/r2_sanitizer.txt records the refusal.
 # compute-sanitizer (memcheck, racecheck, synccheck) over small engine steps that run every launch
 # plan: grouped fused forward + grouped backward, per-rank launches with the fused error-compression
 # + weight-gradient launch, the [wgrad + recurrence] fused plan, the fp32 (3xTF32) tier, and on 2 GPUs
