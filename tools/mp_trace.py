@@ -41,12 +41,12 @@ seq = eng.profile_step()
 t1.record(S)
 torch.cuda.synchronize()
 agg = collections.OrderedDict()
-for name, ms in seq:
+for name, ms, _fl in seq:
     x = agg.setdefault(name, [0, 0.0])
     x[0] += 1
     x[1] += ms * 1e3
 out = {"rank": rank, "step_us": t0.elapsed_time(t1) * 1e3, "calls": {k: [v[0], round(v[1], 1)] for k, v in agg.items()},
-       "seq": [(n, round(ms * 1e3, 1)) for n, ms in seq]}
+       "seq": [(n, round(ms * 1e3, 1)) for n, ms, _f in seq]}
 outs = [None] * world
 if world > 1:
     dist.all_gather_object(outs, out)
