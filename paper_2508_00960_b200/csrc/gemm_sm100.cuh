@@ -119,6 +119,8 @@ struct Epilogue {
   int narrive;       // after each CTA's part of a tile is stored (incl. replicas): fence (system
                      // scope) and add to each arrive[i] (this GPU's and the peers' counters):
   int arrive_units;  //   0: 1 per CTA-tile; 1: rows * cols / 8 of the CTA's part (tiling-independent)
+  int rep_per_half;  // spanning tiles whose two N blocks have different destinations: half h goes to
+                     // out + rep_off[h] (0 = not sent) and counts on arrive[h] (null = none)
   int* arrive[MAX_REP + 1];
   long long rep_off[MAX_REP];   // (peer copies of the output buffer mapped over NVLink: the phantom
                                 // all-gather fused into the compression GEMM's epilogue)
@@ -602,12 +604,13 @@ __device__ __forceinline__ void publisher_loop(const GemmParams& P, int t0, int 
     const int nhalf = pr.nspan > 1 ? 2 : 1;
     const int ncols = pr.nspan > 1 ? pr.nb_extent
                                    : (pr.nb_extent - tc.nin < pr.BN ? pr.nb_extent - tc.nin : pr.BN);
-    int cells = 0;
+    int cells = 0, cells_h[2] = {0, 0};
     for (int h = 0; h < nhalf; ++h) {
       const int q = tc.qn + h;
       if (q >= pr.nblk) break;
       cells += nrows * ncols;
-      if (!E.nrep) continue;
+      cells_h[h] = nrows * ncols;
+      if (!E.nrep || (E.rep_per_half && !E.rep_off[h])) continue;
       const int es = E.out.f32 ? 4 : 2;
       const int upr = ncols * es / 16;
       const long long ldb = E.out.ld * es;
@@ -617,15 +620,23 @@ __device__ __forceinline__ void publisher_loop(const GemmParams& P, int t0, int 
         const int r = u / upr;
         const long long off = r * ldb + (long long)(u - r * upr) * 16;
         const uint4 v = *reinterpret_cast<const uint4*>(src + off);
-        for (int i = 0; i < E.nrep; ++i) *reinterpret_cast<uint4*>(const_cast<char*>(src) + E.rep_off[i] + off) = v;
+        if (E.rep_per_half) *reinterpret_cast<uint4*>(const_cast<char*>(src) + E.rep_off[h] + off) = v;
+        else
+          for (int i = 0; i < E.nrep; ++i) *reinterpret_cast<uint4*>(const_cast<char*>(src) + E.rep_off[i] + off) = v;
       }
     }
     asm volatile("bar.sync 5, 64;" ::: "memory");
     if (E.narrive && tid == 0) {
       __threadfence_system();
-      const int amount = E.arrive_units ? cells / 8 : 1;
-      for (int i = 0; i < E.narrive; ++i)
-        asm volatile("red.relaxed.sys.global.add.s32 [%0], %1;" ::"l"(E.arrive[i]), "r"(amount) : "memory");
+      if (E.rep_per_half) {
+        for (int h = 0; h < 2; ++h)
+          if (E.arrive[h] && cells_h[h])
+            asm volatile("red.relaxed.sys.global.add.s32 [%0], %1;" ::"l"(E.arrive[h]), "r"(cells_h[h] / 8) : "memory");
+      } else {
+        const int amount = E.arrive_units ? cells / 8 : 1;
+        for (int i = 0; i < E.narrive; ++i)
+          asm volatile("red.relaxed.sys.global.add.s32 [%0], %1;" ::"l"(E.arrive[i]), "r"(amount) : "memory");
+      }
     }
   }
 }

@@ -1101,7 +1101,20 @@ static Problem* error_slot_problem(Builder& b, ppx_dtype dt, int32_t n, const pp
   char* local = (char*)contrib + (int64_t)i0 * slot_bytes;
   pr->epi.out = t2(local, f.ldk, dt == PPX_FP32, (int64_t)B * f.ldk);
   if (accumulate) pr->epi.flags |= ppx::EP_ACCUM;
-  if (sc) {
+  if (sc && nslots == 2 && i0 / n != (i0 + 1) / n) {
+    // one logical rank per GPU: the two slots of a pair belong to different owners
+    pr->epi.rep_per_half = 1;
+    pr->epi.arrive_units = 1;
+    for (int h = 0; h < 2; ++h) {
+      const int g = (i0 + h) / n;
+      if (g == sc->rank) continue;          // own slot: stays in contrib (reduced in place)
+      char* dst = (char*)sc->stage[g] + ((int64_t)sc->rank * n + (i0 + h - g * n)) * slot_bytes;
+      pr->epi.rep_off[h] = (long long)(dst - (local + h * slot_bytes));
+      pr->epi.arrive[h] = sc->arrive[g];
+    }
+    pr->epi.nrep = 2;
+    pr->epi.narrive = 2;
+  } else if (sc) {
     const int g = i0 / n;
     if (g != sc->rank) {
       char* dst = (char*)sc->stage[g] + ((int64_t)sc->rank * n + (i0 - g * n)) * slot_bytes;
@@ -1115,9 +1128,12 @@ static Problem* error_slot_problem(Builder& b, ppx_dtype dt, int32_t n, const pp
   return pr;
 }
 
-// slot pairs need bf16 (2-SM tiles), an even slot count per GPU (a pair never straddles two owners)
-// and k a multiple of 64 (each half one whole 64-atom block per CTA)
-static bool error_pairs(ppx_dtype dt, int n, int p, int k) { return dt == PPX_BF16 && n % 2 == 0 && p % 2 == 0 && k % 64 == 0; }
+// slot pairs need bf16 (2-SM tiles), k a multiple of 64 (each half one whole 64-atom block per CTA)
+// and an even number of local ranks (both slots of a pair then share an owner) or exactly one (each
+// half then publishes to its own owner)
+static bool error_pairs(ppx_dtype dt, int n, int p, int k) {
+  return dt == PPX_BF16 && (n % 2 == 0 || n == 1) && p % 2 == 0 && k % 64 == 0;
+}
 
 // Grouped error compression for the n logical ranks one GPU owns (phantom.py:199-205): output
 // slot i = sum over contributing ranks j != i (ascending) of delta_j . D_{i->j}, as ONE
