@@ -1132,7 +1132,9 @@ static Problem* error_slot_problem(Builder& b, ppx_dtype dt, int32_t n, const pp
 // and an even number of local ranks (both slots of a pair then share an owner) or exactly one (each
 // half then publishes to its own owner)
 static bool error_pairs(ppx_dtype dt, int n, int p, int k) {
-  return dt == PPX_BF16 && (n % 2 == 0 || n == 1) && p % 2 == 0 && k % 64 == 0;
+  static const char* ab = getenv("PPX_AB_NO_ERROR_PAIRS");   // A/B of this planner choice only
+  static const bool off = ab && *ab;
+  return !off && dt == PPX_BF16 && (n % 2 == 0 || n == 1) && p % 2 == 0 && k % 64 == 0;
 }
 
 // Grouped error compression for the n logical ranks one GPU owns (phantom.py:199-205): output
