@@ -42,12 +42,13 @@ def to_bytes(v, u):
 def main():
     os.makedirs(P, exist_ok=True)
     md = [f"# Round 2 — B200 evidence (commit {COMMIT})", ""]
-    for src in sorted(glob.glob(os.path.join(G, "ev_bench.json")) + glob.glob(os.path.join(G, "mg_*.json"))):
+    for src in sorted(glob.glob(os.path.join(G, "ev_bench.json")) + glob.glob(os.path.join(G, "mg_c*.json")) +
+                      glob.glob(os.path.join(G, "ev2_*.json"))):
         try:
             line = json.loads(open(src).read().strip().splitlines()[-1])
         except Exception:
             continue
-        name = os.path.basename(src).replace("ev_bench", "c3_n1").replace("mg_", "")
+        name = os.path.basename(src).replace("ev_bench", "c3_n1").replace("mg_", "").replace("ev2_", "")
         json.dump(line, open(os.path.join(P, f"r2_bench_{name}"), "w"), indent=1)
         md.append(f"* `r2_bench_{name}`: value {line.get('value')} {line.get('unit')}, "
                   f"ms/step {line.get('ms_per_step')}, clocks {line.get('clocks', {}).get('sm_mhz')} MHz")
@@ -80,6 +81,13 @@ def main():
                   f"{float(m['gpc__cycles_elapsed.avg.per_second'][0]) * (1000 if m['gpc__cycles_elapsed.avg.per_second'][1] == 'Ghz' else 1):.0f} | "
                   f"{m['sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active'][0]} | {dram / 1e6:.1f} |")
     json.dump(traffic, open(os.path.join(P, "traffic.json"), "w"), indent=1)
+    for f in sorted(glob.glob(os.path.join(G, "cmp_*.json"))):
+        json.dump(json.load(open(f)), open(os.path.join(P, "r2_" + os.path.basename(f)), "w"), indent=1)
+    cli_dir = os.path.join(G, "cmp_cli_acceptance")
+    if os.path.isdir(cli_dir):
+        os.makedirs(os.path.join(P, "r2_cli_compare_acceptance"), exist_ok=True)
+        for f in os.listdir(cli_dir):
+            open(os.path.join(P, "r2_cli_compare_acceptance", f), "w").write(open(os.path.join(cli_dir, f)).read())
     for f in ("epi_ab.txt", "tp_probe.txt", "sanitize_summary.txt", "mgpu_ab.jsonl"):
         if os.path.exists(os.path.join(G, f)):
             md += ["", f"## {f}", "```", open(os.path.join(G, f)).read().rstrip(), "```"]
