@@ -57,17 +57,23 @@ def energy_mj(gpu_index: int) -> float | None:
 
 
 class EnergyMeter:
-    """with EnergyMeter(dev) as m: ... ; m.joules (None without NVML)."""
+    """with EnergyMeter(dev) as m: ... ; m.joules (None without NVML, or when the window was shorter
+    than `min_seconds`: the total-energy counter advances in coarse steps, so sub-second windows
+    read 0 or one whole step)."""
 
-    def __init__(self, gpu_index: int):
-        self.gpu, self.joules = gpu_index, None
+    def __init__(self, gpu_index: int, min_seconds: float = 1.0):
+        self.gpu, self.joules, self.min_seconds = gpu_index, None, min_seconds
 
     def __enter__(self):
+        import time
+        self._t0 = time.perf_counter()
         self._e0 = energy_mj(self.gpu)
         return self
 
     def __exit__(self, *exc):
+        import time
         e1 = energy_mj(self.gpu)
-        if self._e0 is not None and e1 is not None:
+        self.seconds = time.perf_counter() - self._t0
+        if self._e0 is not None and e1 is not None and self.seconds >= self.min_seconds:
             self.joules = (e1 - self._e0) / 1e3
         return False

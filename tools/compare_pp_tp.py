@@ -24,7 +24,7 @@ def main():
     ap.add_argument("--layers", type=int, default=4)
     ap.add_argument("--samples", type=int, default=65536)
     ap.add_argument("--batch", type=int, default=8192)
-    ap.add_argument("--lr", type=float, default=1e-5)
+    ap.add_argument("--lr", type=float, default=3e-6)   # 1e-5 diverges (non-finite) for the PP model at n=8192
     ap.add_argument("--tp-epochs", type=int, default=20)
     ap.add_argument("--max-epochs", type=int, default=200)
     ap.add_argument("--slack", type=float, default=1.05)
