@@ -650,15 +650,22 @@ struct Builder {
       // least-loaded cluster; every role of a cluster walks the same list
       const int sms_avail = ctx->num_sms - ctx->reserved_sms;
       const int C = tiles < sms_avail / 2 ? tiles : sms_avail / 2;
-      // priority problems (prio[i] > 0, e.g. error compression whose outputs other GPUs wait
-      // for) are placed first, so they head every cluster's list
-      std::vector<std::tuple<int, double, int>> cost(tiles);
+      // assignment: plain LPT over all tiles (balance); order within each cluster: priority tiles
+      // (prio[i] > 0, e.g. error compression whose outputs other GPUs wait for) first.  Putting
+      // priority tiles first in the ASSIGNMENT instead would stack them on top of the clusters that
+      // also draw two long tiles (R=1 fused error + weight-gradient launch: 148 vs 128 us)
+      std::vector<std::pair<double, int>> cost(tiles);
+      std::vector<int> tprio(tiles, 0);
+      static const char* ab = getenv("PPX_AB_NO_PRIO");   // A/B of the priority classes only
       for (int i = 0; i < P.nprobs; ++i) {
         const Problem& pr = P.probs[i];
         int kst = 0;
         for (int g = 0; g < pr.nsegs; ++g) kst += pr.segs[g].k_tiles;
         const double c = (kst + 4.0) * pr.BN / 256.0;
-        for (int t = pr.tile_begin; t < pr.tile_begin + ptiles(pr); ++t) cost[t] = {-prio[i], -c, t};
+        for (int t = pr.tile_begin; t < pr.tile_begin + ptiles(pr); ++t) {
+          cost[t] = {-c, t};
+          tprio[t] = (ab && *ab) ? 0 : prio[i];
+        }
       }
       std::stable_sort(cost.begin(), cost.end());
       std::vector<double> load(C, 0.0);
@@ -667,9 +674,11 @@ struct Builder {
         int best = 0;
         for (int c = 1; c < C; ++c)
           if (load[c] < load[best]) best = c;
-        load[best] -= std::get<1>(ct);
-        lists[best].push_back(std::get<2>(ct));
+        load[best] -= ct.first;
+        lists[best].push_back(ct.second);
       }
+      for (auto& l : lists)
+        std::stable_sort(l.begin(), l.end(), [&](int x, int y) { return tprio[x] > tprio[y]; });
       int o = 0;
       for (int c = 0; c < C; ++c) {
         P.sched_off[c] = (uint16_t)o;

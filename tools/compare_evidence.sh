@@ -6,8 +6,10 @@ mkdir -p gpurun_out
 timeout 900 python -m paper_2508_00960_b200 compare --n 256 --p 4 --k 8 --layers 2 --samples 256 --lr 1e-4 \
   --target-loss 4663.4 --max-epochs 1000 --loss-reduction mean --seed 0 --dtype fp32 --out gpurun_out/cmp_cli_acceptance \
   > gpurun_out/cmp_cli.log 2>&1; echo "cli compare rc=$?"
-timeout 1200 python tools/compare_pp_tp.py --out gpurun_out/cmp_b200_n1.json > gpurun_out/cmp_b200_n1.log 2>&1; echo "b200 n1 rc=$?"
+for lr in 1e-6 3e-7; do
+  timeout 1200 python tools/compare_pp_tp.py --lr $lr --out gpurun_out/cmp_b200_n1_lr$lr.json > gpurun_out/cmp_b200_n1_lr$lr.log 2>&1; echo "b200 n1 lr $lr rc=$?"
+done
 if [ "$(nvidia-smi -L | wc -l)" -ge 4 ]; then
   timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29851 \
-    tools/compare_pp_tp.py --out gpurun_out/cmp_b200_n4.json > gpurun_out/cmp_b200_n4.log 2>&1; echo "b200 n4 rc=$?"
+    tools/compare_pp_tp.py --lr 1e-6 --out gpurun_out/cmp_b200_n4.json > gpurun_out/cmp_b200_n4.log 2>&1; echo "b200 n4 rc=$?"
 fi

@@ -56,8 +56,21 @@ def main():
     target = a.slack * tp.loss_history[-1]
     pp_cfg = TrainConfig(mode="pp", p=a.p, k=a.k, max_epochs=a.max_epochs, target_loss=target, optimizer="sgd",
                          **common)
-    pp = train_engine(pp_cfg, data, world=world, rank=rank, device=local, uid=new_uid() if world > 1 else None,
-                      init="device")
+    from paper_2508_00960_b200.errors import TrainingError
+    try:
+        pp = train_engine(pp_cfg, data, world=world, rank=rank, device=local, uid=new_uid() if world > 1 else None,
+                          init="device")
+    except TrainingError as exc:   # the phantom model diverged at this learning rate: say so
+        if rank == 0:
+            line = {"config": {"n": a.n, "p_pp": a.p, "k": a.k, "layers": a.layers, "lr": a.lr, "gpus": world},
+                    "target_loss": target, "tp_loss_history": tp.loss_history, "pp_diverged": str(exc)}
+            print(json.dumps(line))
+            if a.out:
+                json.dump(line, open(a.out, "w"), indent=1)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
 
     def joules(r):
         j = torch.tensor([r.cost["joules"] if r.cost["joules"] is not None else float("nan")], device="cuda")
