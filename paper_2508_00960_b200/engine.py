@@ -21,12 +21,11 @@ from __future__ import annotations
 
 import ctypes
 import math
-import os
 
 import torch
 
 from . import _lib, kernels
-from .core import Activation, as_activation, flat_offsets, round8
+from .core import Activation, as_activation, flat_offsets
 from .errors import ConfigurationError, TrainingError
 from .schedule import local_ranks
 

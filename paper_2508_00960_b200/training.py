@@ -9,7 +9,6 @@ optimizer epilogues and CUDA graphs is engine.PhantomEngine; both call the same 
 
 from __future__ import annotations
 
-import ctypes
 import math
 import time
 from dataclasses import dataclass

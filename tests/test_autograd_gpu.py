@@ -1,9 +1,8 @@
 """PhantomLinearFunction (forward a3, backward a7+a8+a9) through torch.autograd, one rank per
 thread over the in-process Communicator, against the reference's golden gradients (fp32 tier,
 1e-4 normwise, tests/golden/tiny.npz produced by phantomsim itself)."""
-import os
 
-import numpy as np
+
 import pytest
 import torch
 

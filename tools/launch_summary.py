@@ -1,7 +1,7 @@
 """Summarise an ncu `gpu__time_duration.sum` launch list (csv) of `bench.py --steps 1 --warmup 3`:
 picks the last complete training step (the timed graph replay) of our kernels and prints the per-kernel
 share table.  python tools/launch_summary.py launches.csv [launches_per_step]"""
-import collections, csv, io, sys
+import csv, io, sys
 
 txt = open(sys.argv[1]).read()
 rows = [r for r in csv.DictReader(io.StringIO(txt[txt.index('"ID"'):])) if r.get("Metric Name") == "gpu__time_duration.sum"]
