@@ -65,9 +65,14 @@ def peaks():
 
 
 def refuse_debug_knobs():
-    bad = sorted(k for k in os.environ if k.startswith("PPX_DEBUG"))
+    """The bench line is the default launch plan: debug switches (wrong results) and the planner's
+    A/B switches (PPX_AB_*, PPX_NO_*, PPX_QBAL) are refused; only PPX_LIB / PPX_NO_NUMA_BIND pass."""
+    allowed = {"PPX_LIB", "PPX_NO_NUMA_BIND"}
+    bad = sorted(k for k in os.environ if k not in allowed and os.environ[k] != "" and
+                 (k.startswith(("PPX_DEBUG", "PPX_AB_", "PPX_NO_")) or k == "PPX_QBAL"))
     if bad:
-        sys.exit(f"bench.py: refusing to run with debug knobs set ({', '.join(bad)}): they change results")
+        sys.exit(f"bench.py: refusing to run with debug / A-B knobs set ({', '.join(bad)}): the bench measures "
+                 f"the default plan")
 
 
 # ---------------------------------------------------------------------------------------------

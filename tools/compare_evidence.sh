@@ -6,6 +6,7 @@ mkdir -p gpurun_out
 timeout 900 python -m paper_2508_00960_b200 compare --n 256 --p 4 --k 8 --layers 2 --samples 256 --lr 1e-4 \
   --target-loss 4663.4 --max-epochs 1000 --loss-reduction mean --seed 0 --dtype fp32 --out gpurun_out/cmp_cli_acceptance \
   > gpurun_out/cmp_cli.log 2>&1; echo "cli compare rc=$?"
+timeout 1200 python tools/compare_pp_tp.py --lr 1e-6 --k 128 --slack 1.10 --out gpurun_out/cmp_b200_n1_k128.json > gpurun_out/cmp_b200_n1_k128.log 2>&1; echo "b200 n1 k128 rc=$?"
 for lr in 1e-6 3e-7; do
   timeout 1200 python tools/compare_pp_tp.py --lr $lr --out gpurun_out/cmp_b200_n1_lr$lr.json > gpurun_out/cmp_b200_n1_lr$lr.log 2>&1; echo "b200 n1 lr $lr rc=$?"
 done

@@ -13,3 +13,4 @@ timeout 900 python -m pytest tests/test_multigpu_gpu.py -q -rA > gpurun_out/mg_t
 for N in 2 4; do timeout 300 $TR --nproc-per-node $N --master-port $((29820+N)) tools/mp_trace.py --config c3 > gpurun_out/mg_trace_c3_n$N.txt 2>&1; echo "trace n$N rc=$?"; done
 timeout 300 $TR --nproc-per-node 4 --master-port 29830 tools/mp_trace.py --config c2 > gpurun_out/mg_trace_c2_n4.txt 2>&1; echo "trace c2 n4 rc=$?"
 bash tools/compare_evidence.sh > gpurun_out/cmp.log 2>&1
+bash tools/mgpu_ab.sh 4 "c2 c3" 1
