@@ -16,7 +16,7 @@ constexpr int PBK = 128;                         // K elements per stage (2 atom
 constexpr int PSTAGES = 3;
 constexpr int PA_STAGE = BM * 2 * ROW_BYTES;     // 32 KB: [2 K-atoms][128 rows][128 B]
 constexpr int PB_STAGE = 128 * 2 * ROW_BYTES;    // 32 KB: [2 K-atoms][<=128 rows][128 B]
-constexpr int PSMEM_BYTES = PSTAGES * (PA_STAGE + PB_STAGE) + 1024 + 256 + COLSUM_BYTES;
+constexpr int PSMEM_BYTES = PSTAGES * (PA_STAGE + PB_STAGE) + 1024 + 256 + EPI_STAGE_BYTES;
 
 __device__ __forceinline__ void tma4_pair(const CUtensorMap* map, uint32_t bar, uint32_t dst, int c0, int c1, int c2,
                                           int c3) {
@@ -70,8 +70,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  float* cs_smem = reinterpret_cast<float*>(smem_gen + (sBar + 256 - base_u32));
-  for (int i = threadIdx.x; i < 2 * BN_MAX; i += NUM_THREADS) cs_smem[i] = 0.f;
+  uint32_t* epi_stage = reinterpret_cast<uint32_t*>(smem_gen + (sBar + 256 - base_u32));
   const uint32_t crank = cluster_ctarank();
   const bool leader = crank == 0;
   constexpr int CHA = 64;       // bf16 elements per 128-byte atom
@@ -109,7 +108,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
 
   if (is_epi_warp(warp)) {
     reg_alloc_epilogue();
-    epilogue_loop<2 * BM, true>(P, tmem_base, tfull_bar(0), tempty_bar(0), t0, tstep, crank, warp, lane, cs_smem);
+    epilogue_loop<2 * BM, true>(P, tmem_base, tfull_bar(0), tempty_bar(0), t0, tstep, crank, warp, lane, epi_stage);
   } else {
   reg_dealloc_mainloop();
   if (warp >= W_PUB0) {

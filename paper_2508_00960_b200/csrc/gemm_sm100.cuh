@@ -57,8 +57,11 @@ constexpr int MAX_PROBS = 16;
 constexpr int MAX_SEGS = 8;
 constexpr int MAX_REP = 7;
 constexpr int MAX_SCHED = 4096;    // tiles of one LPT-scheduled launch         // peer replicas of an epilogue output (world <= 8)
-constexpr int COLSUM_BYTES = 2 * BN_MAX * 4;     // per-CTA column-sum staging, double-buffered by tile parity
-constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 /*align*/ + 256 /*barriers*/ + COLSUM_BYTES;
+// per-epilogue-warp staging of one 32 x 32 bf16 output chunk (80-byte rows: 64 B data + 16 B pad),
+// so the warp's stores leave as full 64-byte row segments instead of 32 half-filled sectors
+constexpr int EPI_STAGE_ROW_WORDS = 20;
+constexpr int EPI_STAGE_BYTES = NUM_EPI_WARPS * 32 * EPI_STAGE_ROW_WORDS * 4;
+constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 /*align*/ + 256 /*barriers*/ + EPI_STAGE_BYTES;
 
 // epilogue flags
 enum : uint32_t {
@@ -353,6 +356,32 @@ __device__ __forceinline__ void load32(const Tensor2& t, long long off, int nval
   }
 }
 
+// one warp's full 32 x 32 bf16 chunk (rows row0 .. row0+31 of lanes 0..31, columns col .. col+31)
+// through the warp's smem staging: each global store instruction then writes 8 whole 64-byte row
+// segments.  Needs every row and column of the chunk valid and a 16-byte aligned destination.
+__device__ __forceinline__ void store32_bf16_coalesced(uint32_t* stage, const Tensor2& t, long long off_row0, int lane,
+                                                       const float* v) {
+  uint32_t* my = stage + lane * EPI_STAGE_ROW_WORDS;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint4 q;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(v[8 * i + 2 * j], v[8 * i + 2 * j + 1]);
+    *reinterpret_cast<uint4*>(my + 4 * i) = q;
+  }
+  __syncwarp();
+  const int r = lane >> 2, seg = lane & 3;
+  __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(t.ptr) + off_row0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int rr = r + 8 * i;
+    const uint4 q = *reinterpret_cast<const uint4*>(stage + rr * EPI_STAGE_ROW_WORDS + 4 * seg);
+    *reinterpret_cast<uint4*>(base + (long long)rr * t.ld + 8 * seg) = q;
+  }
+  __syncwarp();
+}
+
 __device__ __forceinline__ void store32(const Tensor2& t, long long off, int nvalid, const float* v) {
   if (t.f32) {
     float* p = reinterpret_cast<float*>(t.ptr) + off;
@@ -644,11 +673,13 @@ __device__ __forceinline__ void publisher_loop(const GemmParams& P, int t0, int 
 template <int MT, bool kPair>
 __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem_base, uint32_t tfull0,
                                               uint32_t tempty0, int t0, int tstep, uint32_t crank, int warp,
-                                              int lane, float* cs_smem) {
+                                              int lane, uint32_t* epi_stage) {
   auto tfull_bar = [&](int s) { return tfull0 + 8u * s; };
   auto tempty_bar = [&](int s) { return tempty0 + 8u * s; };
   const int wq = warp & 3;    // TMEM lane quadrant
   const int grp = warp >> 2;  // chunk parity drained by this warp
+  uint32_t* wstage = epi_stage + warp * 32 * EPI_STAGE_ROW_WORDS;
+  const bool coalesce = !(P.dbg & 16);   // A/B (PPX_DEBUG_EPI=scatter): the per-lane row stores
   unsigned long long st_wait = 0, st_busy = 0, st_tmem = 0, st_body = 0;
   int iter = 0;
   for (int t; (t = tile_of(P, t0, tstep, iter)) >= 0; ++iter) {
@@ -818,7 +849,10 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] += (ok(i) && live) ? o[i] : 0.f;
           }
-          if (live) store32(E.out, ooff, nvalid, v);
+          if (F && coalesce && !E.out.f32 && ((reinterpret_cast<uintptr_t>(E.out.ptr) | (E.out.ld * 2) |
+                                                  ((ooff - lane * E.out.ld) * 2)) & 15) == 0)
+            store32_bf16_coalesced(wstage, E.out, ooff - (long long)lane * E.out.ld, lane, v);
+          else if (live) store32(E.out, ooff, nvalid, v);
           if ((flags & EP_BITS) && live) {   // ReLU'(pre) = (y > 0) for the recurrence, 1 bit each
             uint32_t w = 0u;
 #pragma unroll
@@ -885,8 +919,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  float* cs_smem = reinterpret_cast<float*>(smem_gen + (sBar + 256 - base_u32));
-  for (int i = threadIdx.x; i < 2 * BN_MAX; i += NUM_THREADS) cs_smem[i] = 0.f;
+  uint32_t* epi_stage = reinterpret_cast<uint32_t*>(smem_gen + (sBar + 256 - base_u32));
   constexpr int ESIZE = kTF32 ? 4 : 2;
   constexpr int BK = ROW_BYTES / ESIZE;     // elements of K per stage
   constexpr int CH = ROW_BYTES / ESIZE;     // MN-major atom width in elements
@@ -925,7 +958,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
   if (is_epi_warp(warp)) {
     reg_alloc_epilogue();
     epilogue_loop<BM, false>(P, tmem_base, tfull_bar(0), tempty_bar(0), blockIdx.x, gridDim.x, 0u, warp, lane,
-                             cs_smem);
+                             epi_stage);
   } else {
   reg_dealloc_mainloop();
   if (warp >= W_PUB0) {

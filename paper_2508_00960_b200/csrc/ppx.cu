@@ -701,7 +701,8 @@ struct Builder {
     {
       const char* ep = getenv("PPX_DEBUG_EPI");
       P.dbg = (getenv("PPX_DEBUG_NOEPI") ? 1 : 0) | (getenv("PPX_DEBUG_NOWAIT") ? 2 : 0) |
-              (ep && strstr(ep, "mask") ? 4 : 0) | (ep && strstr(ep, "colsum") ? 8 : 0);
+              (ep && strstr(ep, "mask") ? 4 : 0) | (ep && strstr(ep, "colsum") ? 8 : 0) |
+              (ep && strstr(ep, "scatter") ? 16 : 0);
     }
     if (tiles == 0) return PPX_OK;
     cudaError_t e;
