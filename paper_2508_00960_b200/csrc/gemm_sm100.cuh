@@ -819,10 +819,12 @@ __device__ __forceinline__ void epilogue_loop(const GemmParams& P, uint32_t tmem
             tg[i] = ((flags & EP_RELU) && !(v[i] > 0.f)) ? 0.f : diff * E.scale;
             v[i] = y;
           }
-          if (live) {
-            if (E.out.ptr) store32(E.out, ooff, nvalid, v);
-            store32(E.aux, (long long)row * E.aux.ld + col0, nvalid, tg);
-          }
+          if (live && E.out.ptr) store32(E.out, ooff, nvalid, v);
+          const long long aoff = (long long)row * E.aux.ld + col0;
+          if (F && coalesce && !E.aux.f32 && ((reinterpret_cast<uintptr_t>(E.aux.ptr) | (E.aux.ld * 2) |
+                                                ((aoff - lane * E.aux.ld) * 2)) & 15) == 0)
+            store32_bf16_coalesced(wstage, E.aux, aoff - (long long)lane * E.aux.ld, lane, tg);
+          else if (live) store32(E.aux, aoff, nvalid, tg);
           if (flags & EP_COLSUM) {   // bias gradient: one global reduction per column and warp
             const float cs = warp_transpose_sum(tg, lane);
             if (lane < nvalid) atomicAdd(E.colsum + col0 + lane, cs);
