@@ -628,15 +628,22 @@ class PhantomEngine:
         self._launches = 0
         self.trace = []
         st = S.cuda_stream
+        nvtx = torch.cuda.nvtx
+        nvtx.range_push(f"ppx.step[par={par}]")   # host-side NVTX ranges (ncu --nvtx / nsys filters)
         self._call("ppx_hyper_advance", self.hyper.data_ptr(), self.tdev.data_ptr(), float(self.betas[0]),
                    float(self.betas[1]), st)
         self._call("ppx_zero", self.gbias.data_ptr(), self.gbias.numel() * 4, st)
         self._call("ppx_zero", self.loss.data_ptr(), 4, st)
+        nvtx.range_push("ppx.forward")
         self._forward(par, S)
+        nvtx.range_pop()
+        nvtx.range_push("ppx.backward")
         self._backward(par, S)
+        nvtx.range_pop()
         if self.world > 1:
             self._call("ppx_all_reduce_f32", self.loss.data_ptr(), 1, st)
         self.launch_count = self._launches
+        nvtx.range_pop()
 
     # ------------------------------------------------------------------------------------------
     def set_step_count(self, t: int):
