@@ -1,0 +1,6 @@
+#!/bin/bash
+for rep in 1 2 3; do
+  for v in "" scatter; do
+    PPX_DEBUG_EPI=$v timeout 300 python tools/step_time.py --config c3 --steps 40 --reps 2 2>/dev/null | grep config
+  done
+done
