@@ -647,10 +647,12 @@ def time_e2e(eng, D, xs, ts, steps, use_graph, B):
     q0.record(S)
     ready = eng.load_batch_async(xh, th, eng.parity)
     prev_done = None
+    pending = None
     for i in range(steps):
         S.wait_event(ready)
         par = eng.parity
         eng.step(graph=use_graph)
+        loss_i = eng.loss_async()                    # D2H of step i's loss (+ non-finite flag)
         done = torch.cuda.Event()
         done.record(S)
         if i + 1 < steps:
@@ -660,7 +662,10 @@ def time_e2e(eng, D, xs, ts, steps, use_graph, B):
                 eng.copy_stream.wait_event(prev_done)
             ready = eng.load_batch_async(xh, th, 1 - par)
         prev_done = done
-        eng.read_loss()                              # D2H of the step's loss (+ non-finite flag)
+        if pending is not None:
+            pending()                                # the host reads step i-1's loss while step i runs
+        pending = loss_i
+    pending()
     q1.record(S)
     D.barrier()
     te = D.reduce([q0.elapsed_time(q1) / steps])[0]

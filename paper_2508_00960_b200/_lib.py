@@ -83,6 +83,7 @@ _SIGS = {
     "ppx_last_error": (ctypes.c_char_p, [_vp]),
     "ppx_num_sms": (_i32, [_vp]),
     "ppx_reserve_workspace": (_i32, [_vp, _i64]),
+    "ppx_tf32_scope": (_i32, [_vp, _i32, _vp]),
     "ppx_set_reserved_sms": (_i32, [_vp, _i32]),
     "ppx_compress": (_i32, [_vp, _i32, ctypes.POINTER(Layer), _i32, _vp, _i64, _vp, _vp]),
     "ppx_compress_n": (_i32, [_vp, _i32, _i32, ctypes.POINTER(RankIO), _i32, _vp, _vp]),

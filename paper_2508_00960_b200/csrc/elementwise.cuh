@@ -31,45 +31,41 @@ inline int ew_grid(int64_t n, int threads = 256) {
 // ---- 3xTF32 operand split: hi = x with the low 13 mantissa bits cleared, lo = x - hi ----------
 __global__ void split_tf32_kernel(const float* __restrict__ x, float* __restrict__ hi, float* __restrict__ lo,
                                   int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float v = x[i];
-    float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-    hi[i] = h;
-    lo[i] = v - h;
-  }
-}
-inline void launch_split_tf32(const float* x, float* hi, float* lo, int64_t n, cudaStream_t st) {
-  split_tf32_kernel<<<ew_grid(n), 256, 0, st>>>(x, hi, lo, n);
-}
-
-// ---- transposing split: x [slots][rows][cols] (ld, ss) -> hi/lo [slots][cols][rows] (ldo, sso) ----
-// The FP32 tier feeds kind::tf32 only K-major operands (MN-major tf32 operands read as zeros on
-// sm_100a in our measurements), so MN-major fp32 operands are transposed while being split.
-__global__ void split_tf32_t_kernel(const float* __restrict__ x, int rows, int cols, int64_t ld, int64_t ss,
-                                    float* __restrict__ hi, float* __restrict__ lo, int64_t ldo, int64_t sso) {
-  __shared__ float tile[32][33];
-  const int slot = blockIdx.z;
-  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-  const float* xs = x + slot * ss;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    int r = r0 + i, c = c0 + threadIdx.x;
-    tile[i][threadIdx.x] = (r < rows && c < cols) ? xs[(int64_t)r * ld + c] : 0.f;
-  }
-  __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    int c = c0 + i, r = r0 + threadIdx.x;  // output row = c, output col = r
-    if (c < cols && r < rows) {
-      float v = tile[threadIdx.x][i];
-      float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-      hi[slot * sso + (int64_t)c * ldo + r] = h;
-      lo[slot * sso + (int64_t)c * ldo + r] = v - h;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(lo) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(hi) & 15) == 0) {
+    const int64_t n4 = n / 4;
+    for (int64_t i = t0; i < n4; i += stride) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
+      float4 h, l;
+      h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+      h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+      h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+      h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+      l.x = v.x - h.x;
+      l.y = v.y - h.y;
+      l.z = v.z - h.z;
+      l.w = v.w - h.w;
+      reinterpret_cast<float4*>(lo)[i] = l;
+      if (hi) reinterpret_cast<float4*>(hi)[i] = h;
     }
+    for (int64_t i = n4 * 4 + t0; i < n; i += stride) {
+      const float v = x[i], h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+      lo[i] = v - h;
+      if (hi) hi[i] = h;
+    }
+    return;
+  }
+  for (int64_t i = t0; i < n; i += stride) {
+    const float v = x[i], h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    lo[i] = v - h;
+    if (hi) hi[i] = h;
   }
 }
-inline void launch_split_tf32_t(const float* x, int slots, int rows, int cols, int64_t ld, int64_t ss, float* hi,
-                                float* lo, int64_t ldo, int64_t sso, cudaStream_t st) {
-  dim3 grid((cols + 31) / 32, (rows + 31) / 32, slots);
-  split_tf32_t_kernel<<<grid, dim3(32, 8), 0, st>>>(x, rows, cols, ld, ss, hi, lo, ldo, sso);
+// FP32 tier operand split: lo = x - tf32(x) (and, when `hi` is given, hi = tf32(x) explicitly)
+inline void launch_split_tf32(const float* x, float* hi, float* lo, int64_t n, cudaStream_t st) {
+  split_tf32_kernel<<<ew_grid((n + 3) / 4), 256, 0, st>>>(x, hi, lo, n);
 }
 
 // ---- output delta + half-squared loss (phantom.py:169-182, training.py:59-71, 196-199) --------

@@ -54,7 +54,7 @@ __device__ __forceinline__ void reg_dealloc_mainloop() { asm volatile("setmaxnre
 constexpr int TMEM_COLS = 512;    // 2 accumulator stages x 256 fp32 columns
 constexpr int MAX_MAPS = 40;
 constexpr int MAX_PROBS = 16;
-constexpr int MAX_SEGS = 8;
+constexpr int MAX_SEGS = 12;   // 4 contributing ranks x 3 TF32 passes (FP32-tier error slots)
 constexpr int MAX_REP = 7;
 constexpr int MAX_SCHED = 4096;    // tiles of one LPT-scheduled launch         // peer replicas of an epilogue output (world <= 8)
 // per-epilogue-warp staging of one 32 x 32 bf16 output chunk (80-byte rows: 64 B data + 16 B pad),
@@ -251,14 +251,15 @@ __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// UMMA shared-memory descriptor (SWIZZLE_128B, version 1 for sm_100)
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor (version 1 for sm_100): layout 2 = SWIZZLE_128B (16-byte atoms),
+// 1 = SWIZZLE_128B_BASE32B (32-byte atoms, 4-row pattern: the MN-major TF32 operand layout)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
   d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
   d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
   d |= static_cast<uint64_t>(1) << 46;
-  d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+  d |= static_cast<uint64_t>(layout) << 61;
   return d;
 }
 
@@ -1039,10 +1040,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
             for (int kk = 0; kk < NK; ++kk) {
               // MN-major A: atom-major tile (LBO = atom stride, SBO = 1024) or the interleaved
               // canonical tile (LBO = 1024 between MN atoms, SBO = 2 KB between 8-row K groups)
+              // MN-major TF32 (atom-major tile only): 4-row K groups of the 32-byte-atom swizzle
+              // (SBO = 512 B), one MMA = K 8 = two groups
+              constexpr uint32_t MN_SBO = kTF32 ? 512u : 1024u, MN_LAYOUT = kTF32 ? 1u : 2u;
               uint64_t ad = !seg.a.mn ? sdesc(da + kk * 32, 16, 1024)
                             : (seg.a.atoms4d == 2 ? sdesc(da + kk * (KMMA / 8) * (BM / CH) * 1024, 1024, (BM / CH) * 1024)
-                                                  : sdesc(da + kk * (KMMA * ROW_BYTES), BK * ROW_BYTES, 1024));
-              uint64_t bd = seg.b.mn ? sdesc(db + kk * (KMMA * ROW_BYTES), BK * ROW_BYTES, 1024)
+                                                  : sdesc(da + kk * (KMMA * ROW_BYTES), BK * ROW_BYTES, MN_SBO, MN_LAYOUT));
+              uint64_t bd = seg.b.mn ? sdesc(db + kk * (KMMA * ROW_BYTES), BK * ROW_BYTES, MN_SBO, MN_LAYOUT)
                                      : sdesc(db + kk * 32, 16, 1024);
               mma_issue<kTF32>(tmem_d, ad, bd, seg.idesc, accum);
               accum = 1;

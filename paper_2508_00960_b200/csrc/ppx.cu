@@ -37,7 +37,42 @@ struct ppx_ctx {
   std::vector<void*> ipc_mapped;   // ppx_peer_open mappings (cudaIpcCloseMemHandle at destroy)
   unsigned int* fuse_done = nullptr;     // fused launches' CTA exit counter (self-resetting)
   unsigned int* reduce_done = nullptr;   // ppx_reduce_received's block exit counter (self-resetting)
+  // FP32-tier operand cache (ppx_tf32_scope): inside a scope, the 3xTF32 low part of every GEMM
+  // operand read on `lo_stream` is split once and kept across calls until a ppx call writes an
+  // overlapping range (then its buffer returns to the pool)
+  struct LoEntry {
+    int64_t bytes;
+    char* lo;
+    size_t cap;
+  };
+  bool lo_scope = false;
+  cudaStream_t lo_stream = nullptr;
+  std::map<std::pair<const char*, int64_t>, LoEntry> lo_live;   // (operand base, elements) -> low part
+  std::multimap<size_t, char*> lo_pool;                         // free buffers by capacity
+  std::vector<char*> lo_all;
 };
+
+namespace {
+// a ppx call wrote [p, p + bytes): drop the cached low parts of every overlapping operand
+void lo_invalidate(ppx_ctx* ctx, const void* p, int64_t bytes) {
+  if (!ctx || ctx->lo_live.empty() || !p || bytes <= 0) return;
+  const char* a = reinterpret_cast<const char*>(p);
+  for (auto it = ctx->lo_live.begin(); it != ctx->lo_live.end();) {
+    const char* b = it->first.first;
+    if (b < a + bytes && a < b + it->second.bytes) {
+      ctx->lo_pool.insert({it->second.cap, it->second.lo});
+      it = ctx->lo_live.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+void lo_clear(ppx_ctx* ctx) {
+  if (!ctx) return;
+  for (auto& kv : ctx->lo_live) ctx->lo_pool.insert({kv.second.cap, kv.second.lo});
+  ctx->lo_live.clear();
+}
+}  // namespace
 
 namespace {
 
@@ -194,17 +229,22 @@ struct Builder {
   struct MapKey {
     const void* ptr;
     int64_t cols, rows, slots, ld, ss;
-    int bi, br;
+    int bi, br, mn = 0;
     bool operator<(const MapKey& o) const {
-      return std::tie(ptr, cols, rows, slots, ld, ss, bi, br) <
-             std::tie(o.ptr, o.cols, o.rows, o.slots, o.ld, o.ss, o.bi, o.br);
+      return std::tie(ptr, cols, rows, slots, ld, ss, bi, br, mn) <
+             std::tie(o.ptr, o.cols, o.rows, o.slots, o.ld, o.ss, o.bi, o.br, o.mn);
     }
   };
+  // MN-major 32-bit (TF32) operands need the 128B swizzle with 32-byte atoms (the UMMA
+  // SWIZZLE_128B_BASE32B smem layout); everything else uses the 16-byte-atom 128B swizzle
+  CUtensorMapSwizzle swizzle(bool mn) const {
+    return tf32 && mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
+  }
   std::map<MapKey, int> map_cache;
 
-  int add_map(const View& v, int box_inner, int box_rows) {
+  int add_map(const View& v, int box_inner, int box_rows, bool mn) {
     if (!ok()) return 0;
-    MapKey key{v.ptr, v.cols, v.rows, v.slots, v.ld, v.slot_stride, box_inner, box_rows};
+    MapKey key{v.ptr, v.cols, v.rows, v.slots, v.ld, v.slot_stride, box_inner, box_rows, mn ? 1 : 0};
     auto hit = map_cache.find(key);
     if (hit != map_cache.end()) return hit->second;
     if (P.nmaps >= ppx::MAX_MAPS) { error(PPX_E_CONFIG, "too many tensor maps in one launch"); return 0; }
@@ -219,8 +259,7 @@ struct Builder {
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = g_encode(&P.maps[P.nmaps], tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                           3, const_cast<void*>(v.ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                          swizzle(mn), CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
       char msg[256];
       snprintf(msg, sizeof msg, "cuTensorMapEncodeTiled failed (%d): dims %llu,%llu,%llu box %d,%d", (int)r,
@@ -334,8 +373,7 @@ struct Builder {
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = g_encode(&P.maps[P.nmaps], tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                           4, const_cast<void*>(v.ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                          swizzle(true), CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return -1;  // caller falls back to per-atom 3D boxes
     map_cache[key] = P.nmaps;
     return P.nmaps++;
@@ -365,40 +403,67 @@ struct Builder {
     return P.nmaps++;
   }
 
-  // FP32 tier: hi = tf32-truncated x, lo = x - hi over the whole strided extent of the view.
-  // MN-major views are transposed while split and come back K-major (`mn` cleared).
-  std::pair<View, View> split(const View& v, int& mn) {
+  // the scope's cached low part of the operand [base, base + n) (split now on a miss), or null
+  // when no pooled buffer fits and none may be allocated (stream capture): per-call path then
+  char* scoped_lo(const char* base, int64_t n) {
+    auto key = std::make_pair(base, n);
+    auto it = ctx->lo_live.find(key);
+    if (it != ctx->lo_live.end()) return it->second.lo;
+    const size_t bytes = ((size_t)n * 4 + 255) / 256 * 256;
+    char* l = nullptr;
+    size_t cap = 0;
+    auto pit = ctx->lo_pool.lower_bound(bytes);
+    if (pit != ctx->lo_pool.end() && pit->first <= 2 * bytes) {
+      cap = pit->first;
+      l = pit->second;
+      ctx->lo_pool.erase(pit);
+    } else {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+      if (cudaMalloc(&l, bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+      ctx->lo_all.push_back(l);
+      cap = bytes;
+    }
+    ppx::launch_split_tf32(reinterpret_cast<const float*>(base), nullptr, reinterpret_cast<float*>(l), n, st);
+    ctx->lo_live[key] = {n * 4, l, cap};
+    return l;
+  }
+
+  // FP32 tier (3xTF32): x = hi + lo with hi = x with its low 13 mantissa bits cleared and
+  // lo = x - hi, each over the whole strided extent of the view and in the view's own layout
+  // (MN-major views stay MN-major: kind::tf32 reads them through the 32-byte-atom swizzle).
+  // kind::tf32 reads a 32-bit operand with the low 13 bits ignored (checked bit for bit by
+  // tests/test_gemm_gpu.py::test_tf32_raw_hi), so x itself serves as hi and only lo is written;
+  // PPX_AB_TF32_HI_COPY=1 writes the explicit hi copy instead (A/B and that test).
+  std::pair<View, View> split(const View& v) {
     View hi = v, lo = v;
     const int64_t n = (v.slots - 1) * v.slot_stride + (v.rows - 1) * v.ld + v.cols;
-    const bool tr = mn != 0;
-    auto key = std::make_pair(v.ptr, tr ? -n : n);
+    const char* ab = getenv("PPX_AB_TF32_HI_COPY");   // read per call: the raw-hi test flips it
+    const bool hi_copy = ab && *ab && *ab != '0';
+    if (ctx->lo_scope && st == ctx->lo_stream && !hi_copy) {
+      char* l = scoped_lo(reinterpret_cast<const char*>(v.ptr), n);
+      if (l) {
+        lo.ptr = l;
+        return {hi, lo};
+      }
+      if (!ok()) return {hi, lo};
+    }
+    auto key = std::make_pair(v.ptr, n);
     auto it = splits.find(key);
-    int64_t ldo = round8(v.rows), sso = v.cols * ldo;
     void *h = nullptr, *l = nullptr;
     if (it != splits.end()) {
       h = it->second.first;
       l = it->second.second;
     } else {
-      size_t elems = tr ? (size_t)(v.slots * sso) : (size_t)n;
-      size_t bytes = (elems * 4 + 255) / 256 * 256;
-      h = ws_alloc(bytes);
+      const size_t bytes = ((size_t)n * 4 + 255) / 256 * 256;
+      h = hi_copy ? ws_alloc(bytes) : const_cast<void*>(v.ptr);
       l = ws_alloc(bytes);
       if (!h || !l) { error(PPX_E_CUDA, "workspace allocation failed"); return {hi, lo}; }
-      if (tr)
-        ppx::launch_split_tf32_t(reinterpret_cast<const float*>(v.ptr), (int)v.slots, (int)v.rows, (int)v.cols, v.ld,
-                                 v.slot_stride, (float*)h, (float*)l, ldo, sso, st);
-      else
-        ppx::launch_split_tf32(reinterpret_cast<const float*>(v.ptr), (float*)h, (float*)l, n, st);
+      ppx::launch_split_tf32(reinterpret_cast<const float*>(v.ptr), hi_copy ? (float*)h : nullptr, (float*)l, n, st);
       splits[key] = {h, l};
     }
-    if (tr) {
-      hi = View{h, v.rows, v.cols, v.slots, ldo, sso};
-      lo = View{l, v.rows, v.cols, v.slots, ldo, sso};
-      mn = 0;
-    } else {
-      hi.ptr = h;
-      lo.ptr = l;
-    }
+    hi.ptr = h;
+    lo.ptr = l;
     return {hi, lo};
   }
 
@@ -453,13 +518,13 @@ struct Builder {
     if (use_pair) { finalize_pair(pr, a, b, k_tiles, kpb); return; }
     // an MN-major tile is loaded in whole 128-byte atoms: a partial atom would never complete
     // the stage's transaction count
-    if (b.mn && !tf32 && pr->BN % CH) { error(PPX_E_CONFIG, "MN-major B tile width must be a multiple of 64"); return; }
+    if (b.mn && pr->BN % CH) { error(PPX_E_CONFIG, "MN-major B tile width must be a multiple of one 128-byte atom"); return; }
     auto push = [&](const View& av, const View& bv) {
       if (pr->nsegs >= ppx::MAX_SEGS) { error(PPX_E_CONFIG, "too many K segments"); return; }
       Segment& s = pr->segs[pr->nsegs++];
       s.a.atoms4d = 0;
       s.b.atoms4d = 0;
-      if (a.mn && use5d && av.cols % CH == 0) {
+      if (a.mn && use5d && !tf32 && av.cols % CH == 0) {   // 8-row K groups: 16-bit operands only
         int m = add_map5(av, ppx::BM / CH);
         if (m >= 0) { s.a.map = (int8_t)m; s.a.atoms4d = 2; }
       }
@@ -467,7 +532,7 @@ struct Builder {
         int m = add_map4(av, ppx::BM / CH);
         if (m >= 0) { s.a.map = (int8_t)m; s.a.atoms4d = 1; }
       }
-      if (!s.a.atoms4d) s.a.map = (int8_t)(a.mn ? add_map(av, CH, BK) : add_map(av, BK, ppx::BM));
+      if (!s.a.atoms4d) s.a.map = (int8_t)(a.mn ? add_map(av, CH, BK, true) : add_map(av, BK, ppx::BM, false));
       s.a.mn = (int8_t)a.mn;
       s.a.slot_src = (int8_t)a.slot_src;
       s.a.slot_base = a.slot_base;
@@ -476,7 +541,7 @@ struct Builder {
         int m = add_map4(bv, pr->BN / CH);
         if (m >= 0) { s.b.map = (int8_t)m; s.b.atoms4d = 1; }
       }
-      if (!s.b.atoms4d) s.b.map = (int8_t)(b.mn ? add_map(bv, CH, BK) : add_map(bv, BK, pr->BN));
+      if (!s.b.atoms4d) s.b.map = (int8_t)(b.mn ? add_map(bv, CH, BK, true) : add_map(bv, BK, pr->BN, false));
       s.b.mn = (int8_t)b.mn;
       s.b.slot_src = (int8_t)b.slot_src;
       s.b.slot_base = b.slot_base;
@@ -488,8 +553,8 @@ struct Builder {
     if (!tf32) {
       push(a.v, b.v);
     } else {
-      auto as = split(a.v, a.mn);
-      auto bs = split(b.v, b.mn);
+      auto as = split(a.v);
+      auto bs = split(b.v);
       if (!ok()) return;
       push(as.second, bs.first);  // lo * hi
       push(as.first, bs.second);  // hi * lo
@@ -731,7 +796,24 @@ struct Builder {
     }
     if (e != cudaSuccess) return fail(ctx, PPX_E_CUDA, "gemm launch: %s", cudaGetErrorString(e));
     dbg_pending("after gemm launch");
+    invalidate_outputs();
     return PPX_OK;
+  }
+
+  // the FP32-tier operand cache forgets every operand this launch's epilogues write (a generous
+  // extent: all rows up to the problem's last, every slot)
+  void invalidate_outputs() {
+    if (ctx->lo_live.empty()) return;
+    for (int i = 0; i < P.nprobs; ++i) {
+      const Problem& pr = P.probs[i];
+      const ppx::Epilogue& E = pr.epi;
+      const int64_t rows = pr.m_base + pr.M, slots = pr.nblk + 2;
+      for (const ppx::Tensor2* t : {&E.out, &E.aux, &E.preact, &E.master, &E.adam_m, &E.adam_v}) {
+        if (!t->ptr) continue;
+        const int64_t es = t->f32 ? 4 : 2;
+        lo_invalidate(ctx, t->ptr, (rows * t->ld + slots * t->slot_stride + pr.nb_extent) * es);
+      }
+    }
   }
 };
 
@@ -840,6 +922,7 @@ ppx_status ppx_destroy(ppx_ctx* ctx) {
   if (!ctx) return PPX_OK;
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (auto& c : ctx->ws) cudaFree(c.first);
+  for (char* m : ctx->lo_all) cudaFree(m);
   for (void* m : ctx->ipc_mapped) cudaIpcCloseMemHandle(m);
   if (ctx->fuse_done) cudaFree(ctx->fuse_done);
   if (ctx->reduce_done) cudaFree(ctx->reduce_done);
@@ -1044,6 +1127,7 @@ ppx_status ppx_output_delta(ppx_ctx* ctx, ppx_dtype dt, int32_t B, int32_t s, pp
   if (!ctx) return PPX_E_CONFIG;
   if (B < 1 || s < 1 || !y_out || !target || !delta || (act == PPX_RELU && !pre))
     return fail(ctx, PPX_E_CONFIG, "ppx_output_delta: bad arguments");
+  lo_invalidate(ctx, delta, (int64_t)B * ld_d * (dt == PPX_FP32 ? 4 : 2));
   cudaError_t e = ppx::launch_output_delta(dt == PPX_FP32, B, s, act == PPX_RELU, y_out, ld_y, target, ld_t, pre, ld_p,
                                            delta, ld_d, delta_scale, loss_scale, loss, (cudaStream_t)stream);
   return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "output_delta: %s", cudaGetErrorString(e));
@@ -1152,7 +1236,8 @@ static bool error_pairs(ppx_dtype dt, int n, int p, int k) {
 // K-concatenated problem per slot (segment j reads D_{i->j} = slot i - (i > j) of rank j's
 // decompressor stack), so the ranks' contributions are summed in the fp32 accumulator instead
 // of n accumulate launches.  Slots without a contributor are not written.  Falls back to the
-// per-rank accumulate launches when a slot would need more than MAX_SEGS segments (or 3xTF32).
+// per-rank accumulate launches when a slot would need more than MAX_SEGS segments (3 per
+// contributing rank in the 3xTF32 tier).
 ppx_status ppx_error_phantoms_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx_rank_io* io, int32_t B,
                                 void* contrib, void* stream) {
   if (!ctx) return PPX_E_CONFIG;
@@ -1167,7 +1252,7 @@ ppx_status ppx_error_phantoms_n(ppx_ctx* ctx, ppx_dtype dt, int32_t n, const ppx
   if (p < 2) return PPX_OK;
   Flat f(s, k, p);
   const int es = dt == PPX_FP32 ? 4 : 2;
-  if (n == 1 || dt == PPX_FP32 || n > ppx::MAX_SEGS) {
+  if (n == 1 || n * (dt == PPX_FP32 ? 3 : 1) > ppx::MAX_SEGS) {
     if (n > 1) {
       cudaError_t e = cudaMemsetAsync(contrib, 0, (size_t)p * B * f.ldk * es, (cudaStream_t)stream);
       if (e != cudaSuccess) return fail(ctx, PPX_E_CUDA, "error_phantoms_n: %s", cudaGetErrorString(e));
@@ -1263,6 +1348,7 @@ ppx_status ppx_reduce_received(ppx_ctx* ctx, ppx_dtype dt, int32_t R, int64_t sl
       slot_elems % 8 || dt != PPX_BF16)
     return fail(ctx, PPX_E_CONFIG, "ppx_reduce_received: bad arguments");
   if (!ctx->reduce_done) return fail(ctx, PPX_E_SEQUENCING, "ppx_reduce_received before ppx_peer_alloc");
+  lo_invalidate(ctx, out, (int64_t)R * slot_elems * 2);
   ppx::ReduceArgs a;
   a.stage = (const __nv_bfloat16*)stage;
   a.own = (const __nv_bfloat16*)own;
@@ -1290,6 +1376,7 @@ ppx_status ppx_all_gather(ppx_ctx* ctx, ppx_dtype dt, void* phantoms, int64_t sl
   const int64_t chunk = slot_elems * local_ranks;
   char* base = (char*)phantoms;
   const int es = dt == PPX_FP32 ? 4 : 2;
+  lo_invalidate(ctx, base, chunk * ctx->world * es);
   NCCL_TRY(ctx, ncclAllGather(base + (int64_t)ctx->rank * chunk * es, base, (size_t)chunk, nccl_type(dt), ctx->comm,
                               (cudaStream_t)stream));
   return PPX_OK;
@@ -1302,6 +1389,7 @@ ppx_status ppx_reduce_scatter(ppx_ctx* ctx, ppx_dtype dt, void* contrib, int64_t
   const int64_t chunk = slot_elems * local_ranks;
   char* base = (char*)contrib;
   const int es = dt == PPX_FP32 ? 4 : 2;
+  lo_invalidate(ctx, base, chunk * ctx->world * es);
   NCCL_TRY(ctx, ncclReduceScatter(base, base + (int64_t)ctx->rank * chunk * es, (size_t)chunk, nccl_type(dt), ncclSum,
                                   ctx->comm, (cudaStream_t)stream));
   return PPX_OK;
@@ -1312,6 +1400,7 @@ ppx_status ppx_reduce_scatter_to(ppx_ctx* ctx, ppx_dtype dt, const void* contrib
   if (!ctx || !contrib || !recv) return PPX_E_CONFIG;
   const int64_t chunk = slot_elems * local_ranks;
   const int es = dt == PPX_FP32 ? 4 : 2;
+  lo_invalidate(ctx, recv, chunk * es);
   if (ctx->world == 1) {
     CUDA_TRY(ctx, cudaMemcpyAsync(recv, contrib, (size_t)(chunk * es), cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
     return PPX_OK;
@@ -1322,6 +1411,7 @@ ppx_status ppx_reduce_scatter_to(ppx_ctx* ctx, ppx_dtype dt, const void* contrib
 
 ppx_status ppx_all_reduce_f32(ppx_ctx* ctx, float* buf, int64_t count, void* stream) {
   if (!ctx) return PPX_E_CONFIG;
+  lo_invalidate(ctx, buf, count * 4);
   if (ctx->world == 1) return PPX_OK;
   NCCL_TRY(ctx, ncclAllReduce(buf, buf, (size_t)count, ncclFloat32, ncclSum, ctx->comm, (cudaStream_t)stream));
   return PPX_OK;
@@ -1329,6 +1419,7 @@ ppx_status ppx_all_reduce_f32(ppx_ctx* ctx, float* buf, int64_t count, void* str
 
 ppx_status ppx_all_reduce(ppx_ctx* ctx, ppx_dtype dt, void* buf, int64_t count, void* stream) {
   if (!ctx) return PPX_E_CONFIG;
+  lo_invalidate(ctx, buf, count * (dt == PPX_FP32 ? 4 : 2));
   if (ctx->world == 1) return PPX_OK;
   NCCL_TRY(ctx, ncclAllReduce(buf, buf, (size_t)count, nccl_type(dt), ncclSum, ctx->comm, (cudaStream_t)stream));
   return PPX_OK;
@@ -1604,6 +1695,7 @@ ppx_status ppx_colsum(ppx_ctx* ctx, ppx_dtype dt, int32_t rows, int32_t cols, co
                       int32_t accumulate, void* stream) {
   if (!ctx) return PPX_E_CONFIG;
   if (rows < 1 || cols < 1 || !x || !out) return fail(ctx, PPX_E_CONFIG, "ppx_colsum: bad arguments");
+  lo_invalidate(ctx, out, (int64_t)cols * 4);
   cudaError_t e = ppx::launch_colsum(dt == PPX_FP32, rows, cols, x, ld, out, accumulate, (cudaStream_t)stream);
   return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "colsum: %s", cudaGetErrorString(e));
 }
@@ -1617,6 +1709,7 @@ ppx_status ppx_optimizer_step(ppx_ctx* ctx, int32_t kind, const float* hyper, fl
       (kind != PPX_UPDATE_SGD && kind != PPX_UPDATE_ADAM))
     return fail(ctx, PPX_E_CONFIG, "ppx_optimizer_step: bad arguments");
   if (n == 0) return PPX_OK;
+  lo_clear(ctx);
   cudaError_t e = ppx::launch_optimizer(kind == PPX_UPDATE_ADAM, hyper, params, grad, adam_m, adam_v, n,
                                         dt == PPX_FP32, w_copy, bad, (cudaStream_t)stream);
   return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "optimizer: %s", cudaGetErrorString(e));
@@ -1625,6 +1718,8 @@ ppx_status ppx_optimizer_step(ppx_ctx* ctx, int32_t kind, const float* hyper, fl
 ppx_status ppx_hyper_advance(ppx_ctx* ctx, float* hyper, int32_t* step, double beta1, double beta2, void* stream) {
   if (!ctx) return PPX_E_CONFIG;
   if (!hyper || !step) return fail(ctx, PPX_E_CONFIG, "ppx_hyper_advance: bad arguments");
+  lo_invalidate(ctx, hyper, 6 * 4);
+  lo_invalidate(ctx, step, 4);
   cudaError_t e = ppx::launch_hyper_advance(hyper, step, beta1, beta2, (cudaStream_t)stream);
   return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "hyper_advance: %s", cudaGetErrorString(e));
 }
@@ -1677,10 +1772,19 @@ ppx_status ppx_gemm_update(ppx_ctx* ctx, ppx_dtype dt, int32_t M, int32_t N, int
   return b.launch();
 }
 
+ppx_status ppx_tf32_scope(ppx_ctx* ctx, int32_t on, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  lo_clear(ctx);
+  ctx->lo_scope = on != 0;
+  ctx->lo_stream = (cudaStream_t)stream;
+  return PPX_OK;
+}
+
 ppx_status ppx_zero(ppx_ctx* ctx, void* ptr, int64_t bytes, void* stream) {
   if (!ctx) return PPX_E_CONFIG;
   if (bytes < 0 || (bytes > 0 && !ptr)) return fail(ctx, PPX_E_CONFIG, "ppx_zero: bad arguments");
   if (bytes == 0) return PPX_OK;
+  lo_invalidate(ctx, ptr, bytes);
   CUDA_TRY(ctx, cudaMemsetAsync(ptr, 0, (size_t)bytes, (cudaStream_t)stream));
   return PPX_OK;
 }
@@ -1690,6 +1794,7 @@ ppx_status ppx_cast(ppx_ctx* ctx, ppx_dtype src_dt, const void* src, ppx_dtype d
   if (!ctx) return PPX_E_CONFIG;
   if (n < 0 || (n > 0 && (!src || !dst))) return fail(ctx, PPX_E_CONFIG, "ppx_cast: bad arguments");
   if (n == 0) return PPX_OK;
+  lo_invalidate(ctx, dst, n * (dst_dt == PPX_FP32 ? 4 : 2));
   cudaError_t e = ppx::launch_cast(src_dt == PPX_FP32, src, dst_dt == PPX_FP32, dst, n, (cudaStream_t)stream);
   return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "cast: %s", cudaGetErrorString(e));
 }
@@ -1698,6 +1803,7 @@ ppx_status ppx_bias_act(ppx_ctx* ctx, ppx_dtype dt, int32_t rows, int32_t cols, 
                         const float* bias, ppx_act act, void* y, int64_t ldy, void* stream) {
   if (!ctx) return PPX_E_CONFIG;
   if (rows < 1 || cols < 1 || !x || !y) return fail(ctx, PPX_E_CONFIG, "ppx_bias_act: bad arguments");
+  lo_clear(ctx);
   cudaError_t e = ppx::launch_bias_act(dt == PPX_FP32, rows, cols, x, ldx, bias, act == PPX_RELU, y, ldy,
                                        (cudaStream_t)stream);
   return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "bias_act: %s", cudaGetErrorString(e));
@@ -1707,6 +1813,7 @@ ppx_status ppx_relu_mask(ppx_ctx* ctx, ppx_dtype dt, int32_t rows, int32_t cols,
                          const void* mask_src, int64_t ldm, void* stream) {
   if (!ctx) return PPX_E_CONFIG;
   if (rows < 1 || cols < 1 || !x || !mask_src) return fail(ctx, PPX_E_CONFIG, "ppx_relu_mask: bad arguments");
+  lo_clear(ctx);
   cudaError_t e = ppx::launch_relu_mask(dt == PPX_FP32, rows, cols, x, ldx, mask_src, ldm, (cudaStream_t)stream);
   return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "relu_mask: %s", cudaGetErrorString(e));
 }

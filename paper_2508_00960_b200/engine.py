@@ -174,6 +174,10 @@ class PhantomEngine:
         self.tdev = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.out_host = torch.zeros(1, dtype=f32).pin_memory()
         self.bad_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+        # loss_async(): ring of pinned (loss, flag) slots for reads that lag the steps
+        self._loss_ring = [(torch.zeros(1, dtype=f32).pin_memory(), torch.zeros(1, dtype=torch.int32).pin_memory())
+                           for _ in range(4)]
+        self._loss_i = 0
         if dtype == torch.float32:   # 3xTF32 hi/lo splits: reserve so graph capture never allocates
             per_call = 4 * B * s + 2 * p * B * ldk + 2 * T + 4 * s * ldk
             self.ctx.call("ppx_reserve_workspace", int(2 * 4 * per_call * 1.25) + (1 << 20))
@@ -630,6 +634,7 @@ class PhantomEngine:
         st = S.cuda_stream
         nvtx = torch.cuda.nvtx
         nvtx.range_push(f"ppx.step[par={par}]")   # host-side NVTX ranges (ncu --nvtx / nsys filters)
+        self._tf32_scope(1, st)
         self._call("ppx_hyper_advance", self.hyper.data_ptr(), self.tdev.data_ptr(), float(self.betas[0]),
                    float(self.betas[1]), st)
         self._call("ppx_zero", self.gbias.data_ptr(), self.gbias.numel() * 4, st)
@@ -642,8 +647,15 @@ class PhantomEngine:
         nvtx.range_pop()
         if self.world > 1:
             self._call("ppx_all_reduce_f32", self.loss.data_ptr(), 1, st)
+        self._tf32_scope(0, st)
         self.launch_count = self._launches
         nvtx.range_pop()
+
+    def _tf32_scope(self, on, st):
+        """FP32 tier: inside one step every GEMM operand's 3xTF32 low part is split once and reused
+        across calls (ppx_tf32_scope); nothing but ppx calls writes engine buffers in a step."""
+        if self.dtype == torch.float32:
+            self.ctx.call("ppx_tf32_scope", int(on), st)
 
     # ------------------------------------------------------------------------------------------
     def set_step_count(self, t: int):
@@ -727,7 +739,10 @@ class PhantomEngine:
         else:
             self._keep.clear()
             self._launches = 0
-            self._forward(par, torch.cuda.current_stream(), train=False)
+            st = torch.cuda.current_stream()
+            self._tf32_scope(1, st.cuda_stream)
+            self._forward(par, st, train=False)
+            self._tf32_scope(0, st.cuda_stream)
             self.infer_launch_count = self._launches
         return [self.Y[par][jj][self.L] for jj in range(self.R)]
 
@@ -741,7 +756,10 @@ class PhantomEngine:
             with torch.cuda.graph(g, stream=cs):
                 self._keep.clear()
                 self._launches = 0
-                self._forward(par, torch.cuda.current_stream(), train=False)
+                st = torch.cuda.current_stream()
+                self._tf32_scope(1, st.cuda_stream)
+                self._forward(par, st, train=False)
+                self._tf32_scope(0, st.cuda_stream)
                 self.infer_launch_count = self._launches
             self.infer_graphs[par] = g
         torch.cuda.synchronize()
@@ -765,12 +783,35 @@ class PhantomEngine:
             ev.record(self.copy_stream)
         return ev
 
+    @staticmethod
+    def _check_flag(flag: int):
+        if flag & 2:
+            raise TrainingError("a peer GPU never published its phantoms (NVLink exchange / fused wait timed out)")
+        if flag != 0:
+            raise TrainingError("non-finite gradient detected on the device")
+
     def read_loss(self) -> float:
         self.out_host.copy_(self.loss, non_blocking=True)
         self.bad_host.copy_(self.bad, non_blocking=True)
         torch.cuda.current_stream().synchronize()
-        if int(self.bad_host[0]) & 2:
-            raise TrainingError("a peer GPU never published its phantoms (NVLink exchange / fused wait timed out)")
-        if int(self.bad_host[0]) != 0:
-            raise TrainingError("non-finite gradient detected on the device")
+        self._check_flag(int(self.bad_host[0]))
         return float(self.out_host[0].item())
+
+    def loss_async(self):
+        """Enqueue the D2H read of the last step's loss (and non-finite flag) on the current
+        stream without waiting; returns a function that waits for that copy only and returns the
+        loss (raising TrainingError like read_loss).  A training loop that calls it after step i
+        and resolves it after enqueuing step i + 1 keeps the GPU fed while still reading every
+        step's loss.  At most 4 reads may be pending at once."""
+        self._loss_i = (self._loss_i + 1) % len(self._loss_ring)
+        lh, bh = self._loss_ring[self._loss_i]
+        lh.copy_(self.loss, non_blocking=True)
+        bh.copy_(self.bad, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+
+        def result() -> float:
+            ev.synchronize()
+            self._check_flag(int(bh[0]))
+            return float(lh[0].item())
+        return result

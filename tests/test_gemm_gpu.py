@@ -39,6 +39,31 @@ def test_gemm_layouts(dtype, ta, tb, shape):
     assert err.item() < tol, f"normwise error {err.item():.3e}"
 
 
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("tb", [False, True])
+def test_tf32_raw_hi(ta, tb, monkeypatch):
+    """The FP32 tier passes x itself as the 'hi' operand of 3xTF32 (kind::tf32 ignores the low 13
+    mantissa bits): bit-identical to an explicit truncated hi copy (PPX_AB_TF32_HI_COPY=1), and
+    fp32-accurate vs float64, on full-mantissa inputs in every operand majorness (MN-major TF32
+    tiles use the 32-byte-atom swizzle)."""
+    from paper_2508_00960_b200 import kernels
+    M, N, K = 384, 320, 1000
+    g = torch.Generator(device="cuda").manual_seed(11 + 2 * ta + tb)
+    a = torch.randn(K, M, device="cuda", generator=g) if ta else torch.randn(M, K, device="cuda", generator=g)
+    b = torch.randn(N, K, device="cuda", generator=g) if tb else torch.randn(K, N, device="cuda", generator=g)
+    outs = []
+    for copy in ("0", "1"):
+        monkeypatch.setenv("PPX_AB_TF32_HI_COPY", copy)
+        out = torch.empty(M, N, device="cuda", dtype=torch.float32)
+        kernels.gemm(a, b, ta, tb, out=out)
+        torch.cuda.synchronize()
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1]), "raw-hi and explicit-hi 3xTF32 differ"
+    ref = (a.double().t() if ta else a.double()) @ (b.double().t() if tb else b.double())
+    err = ((outs[0].double() - ref).norm() / ref.norm()).item()
+    assert err < 1e-5, f"3xTF32 normwise error {err:.3e}"   # fp32 accumulation over K = 1000: ~3e-6
+
+
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
 @pytest.mark.parametrize("s,k,p,R,B", [(256, 128, 8, 8, 512), (256, 128, 8, 3, 256), (128, 32, 4, 4, 64),
                                        (256, 64, 4, 2, 200), (192, 128, 8, 1, 256), (256, 128, 8, 4, 256),
