@@ -107,6 +107,9 @@ ppx_status ppx_create(int32_t world, int32_t rank, int32_t device, const uint8_t
 ppx_status ppx_destroy(ppx_ctx* ctx);
 const char* ppx_last_error(const ppx_ctx* ctx);
 int32_t ppx_num_sms(const ppx_ctx* ctx);
+/* Kernels this context has enqueued so far (GEMMs, TF32 splits, elementwise helpers; not NCCL,
+   not memsets): the engine's per-step launch count (bench.py `gpu_launches`). */
+int64_t ppx_kernel_launches(const ppx_ctx* ctx);
 /* GEMM launches issued while this is non-zero leave `n` SMs free, so a collective running on
    another stream (NCCL needs SMs of its own) can progress under the GEMM. */
 ppx_status ppx_set_reserved_sms(ppx_ctx* ctx, int32_t n);

@@ -82,6 +82,7 @@ _SIGS = {
     "ppx_destroy": (_i32, [_vp]),
     "ppx_last_error": (ctypes.c_char_p, [_vp]),
     "ppx_num_sms": (_i32, [_vp]),
+    "ppx_kernel_launches": (_i64, [_vp]),
     "ppx_reserve_workspace": (_i32, [_vp, _i64]),
     "ppx_tf32_scope": (_i32, [_vp, _i32, _vp]),
     "ppx_set_reserved_sms": (_i32, [_vp, _i32]),
@@ -207,6 +208,11 @@ class Context:
     @property
     def num_sms(self) -> int:
         return load().ppx_num_sms(self.handle)
+
+    @property
+    def kernel_launches(self) -> int:
+        """Kernels this context has enqueued (GEMMs, TF32 splits, elementwise helpers)."""
+        return int(load().ppx_kernel_launches(self.handle))
 
     def close(self):
         if getattr(self, "handle", None):

@@ -45,6 +45,7 @@ struct ppx_ctx {
     char* lo;
     size_t cap;
   };
+  long long launches = 0;   // kernels this context enqueued (ppx_kernel_launches)
   bool lo_scope = false;
   cudaStream_t lo_stream = nullptr;
   std::map<std::pair<const char*, int64_t>, LoEntry> lo_live;   // (operand base, elements) -> low part
@@ -425,6 +426,7 @@ struct Builder {
       cap = bytes;
     }
     ppx::launch_split_tf32(reinterpret_cast<const float*>(base), nullptr, reinterpret_cast<float*>(l), n, st);
+    ++ctx->launches;
     ctx->lo_live[key] = {n * 4, l, cap};
     return l;
   }
@@ -460,6 +462,7 @@ struct Builder {
       l = ws_alloc(bytes);
       if (!h || !l) { error(PPX_E_CUDA, "workspace allocation failed"); return {hi, lo}; }
       ppx::launch_split_tf32(reinterpret_cast<const float*>(v.ptr), hi_copy ? (float*)h : nullptr, (float*)l, n, st);
+      ++ctx->launches;
       splits[key] = {h, l};
     }
     hi.ptr = h;
@@ -795,23 +798,30 @@ struct Builder {
       e = tf32 ? ppx::launch_gemm<true>(P, grid, st) : ppx::launch_gemm<false>(P, grid, st);
     }
     if (e != cudaSuccess) return fail(ctx, PPX_E_CUDA, "gemm launch: %s", cudaGetErrorString(e));
+    ++ctx->launches;
     dbg_pending("after gemm launch");
     invalidate_outputs();
     return PPX_OK;
   }
 
-  // the FP32-tier operand cache forgets every operand this launch's epilogues write (a generous
-  // extent: all rows up to the problem's last, every slot)
+  // the FP32-tier operand cache forgets every operand this launch's epilogues write: the span
+  // from row 0 to the last element of the problem's last row and slot (peer replicas included)
   void invalidate_outputs() {
     if (ctx->lo_live.empty()) return;
     for (int i = 0; i < P.nprobs; ++i) {
       const Problem& pr = P.probs[i];
       const ppx::Epilogue& E = pr.epi;
-      const int64_t rows = pr.m_base + pr.M, slots = pr.nblk + 2;
+      const int64_t last_row = pr.m_base + pr.M - 1;
+      const int64_t last_slot = pr.nblk - 1 + (E.out_skip != INT_MAX ? 1 : 0);
       for (const ppx::Tensor2* t : {&E.out, &E.aux, &E.preact, &E.master, &E.adam_m, &E.adam_v}) {
         if (!t->ptr) continue;
-        const int64_t es = t->f32 ? 4 : 2;
-        lo_invalidate(ctx, t->ptr, (rows * t->ld + slots * t->slot_stride + pr.nb_extent) * es);
+        const bool words = t == &E.preact && (E.flags & ppx::EP_BITS);   // 1-bit masks in uint32 words
+        const int64_t es = words ? 4 : (t->f32 ? 4 : 2);
+        const int64_t cols = words ? (pr.nb_extent + 31) / 32 : pr.nb_extent;
+        const int64_t bytes = (last_row * t->ld + last_slot * t->slot_stride + cols) * es;
+        lo_invalidate(ctx, t->ptr, bytes);
+        if (t == &E.out)
+          for (int r = 0; r < E.nrep; ++r) lo_invalidate(ctx, (const char*)t->ptr + E.rep_off[r], bytes);
       }
     }
   }
@@ -933,6 +943,7 @@ ppx_status ppx_destroy(ppx_ctx* ctx) {
 
 const char* ppx_last_error(const ppx_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 int32_t ppx_num_sms(const ppx_ctx* ctx) { return ctx ? ctx->num_sms : 0; }
+int64_t ppx_kernel_launches(const ppx_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 ppx_status ppx_set_reserved_sms(ppx_ctx* ctx, int32_t n) {
   if (!ctx || n < 0 || n > ctx->num_sms - 2) return PPX_E_CONFIG;
@@ -1128,6 +1139,7 @@ ppx_status ppx_output_delta(ppx_ctx* ctx, ppx_dtype dt, int32_t B, int32_t s, pp
   if (B < 1 || s < 1 || !y_out || !target || !delta || (act == PPX_RELU && !pre))
     return fail(ctx, PPX_E_CONFIG, "ppx_output_delta: bad arguments");
   lo_invalidate(ctx, delta, (int64_t)B * ld_d * (dt == PPX_FP32 ? 4 : 2));
+  ++ctx->launches;
   cudaError_t e = ppx::launch_output_delta(dt == PPX_FP32, B, s, act == PPX_RELU, y_out, ld_y, target, ld_t, pre, ld_p,
                                            delta, ld_d, delta_scale, loss_scale, loss, (cudaStream_t)stream);
   return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "output_delta: %s", cudaGetErrorString(e));
@@ -1363,6 +1375,7 @@ ppx_status ppx_reduce_received(ppx_ctx* ctx, ppx_dtype dt, int32_t R, int64_t sl
   a.per_epoch = (int)((int64_t)(world - 1) * R * slot_elems / 8);
   a.bad = bad;
   a.done = ctx->reduce_done;
+  ++ctx->launches;
   CUDA_TRY(ctx, ppx::launch_reduce_received(a, (cudaStream_t)stream));
   return PPX_OK;
 }
@@ -1512,6 +1525,7 @@ static ppx_status wgrad_add(ppx_ctx* ctx, ppx_dtype dt, Builder& b, const ppx_wg
 static ppx_status wgrad_bias(ppx_ctx* ctx, ppx_dtype dt, const ppx_wgrad_item& it, cudaStream_t st) {
   if (!(it.parts & PPX_GRAD_BIAS) || !it.grad) return PPX_OK;
   Flat f(it.layer->s, it.layer->k, it.layer->p);
+  ++ctx->launches;
   cudaError_t e = ppx::launch_colsum(dt == PPX_FP32, it.B, it.layer->s, it.delta, it.ld_d, it.grad + f.bias, 0, st);
   return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "colsum: %s", cudaGetErrorString(e));
 }
@@ -1696,6 +1710,7 @@ ppx_status ppx_colsum(ppx_ctx* ctx, ppx_dtype dt, int32_t rows, int32_t cols, co
   if (!ctx) return PPX_E_CONFIG;
   if (rows < 1 || cols < 1 || !x || !out) return fail(ctx, PPX_E_CONFIG, "ppx_colsum: bad arguments");
   lo_invalidate(ctx, out, (int64_t)cols * 4);
+  ++ctx->launches;
   cudaError_t e = ppx::launch_colsum(dt == PPX_FP32, rows, cols, x, ld, out, accumulate, (cudaStream_t)stream);
   return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "colsum: %s", cudaGetErrorString(e));
 }
@@ -1710,6 +1725,7 @@ ppx_status ppx_optimizer_step(ppx_ctx* ctx, int32_t kind, const float* hyper, fl
     return fail(ctx, PPX_E_CONFIG, "ppx_optimizer_step: bad arguments");
   if (n == 0) return PPX_OK;
   lo_clear(ctx);
+  ++ctx->launches;
   cudaError_t e = ppx::launch_optimizer(kind == PPX_UPDATE_ADAM, hyper, params, grad, adam_m, adam_v, n,
                                         dt == PPX_FP32, w_copy, bad, (cudaStream_t)stream);
   return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "optimizer: %s", cudaGetErrorString(e));
@@ -1720,6 +1736,7 @@ ppx_status ppx_hyper_advance(ppx_ctx* ctx, float* hyper, int32_t* step, double b
   if (!hyper || !step) return fail(ctx, PPX_E_CONFIG, "ppx_hyper_advance: bad arguments");
   lo_invalidate(ctx, hyper, 6 * 4);
   lo_invalidate(ctx, step, 4);
+  ++ctx->launches;
   cudaError_t e = ppx::launch_hyper_advance(hyper, step, beta1, beta2, (cudaStream_t)stream);
   return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "hyper_advance: %s", cudaGetErrorString(e));
 }
@@ -1795,6 +1812,7 @@ ppx_status ppx_cast(ppx_ctx* ctx, ppx_dtype src_dt, const void* src, ppx_dtype d
   if (n < 0 || (n > 0 && (!src || !dst))) return fail(ctx, PPX_E_CONFIG, "ppx_cast: bad arguments");
   if (n == 0) return PPX_OK;
   lo_invalidate(ctx, dst, n * (dst_dt == PPX_FP32 ? 4 : 2));
+  ++ctx->launches;
   cudaError_t e = ppx::launch_cast(src_dt == PPX_FP32, src, dst_dt == PPX_FP32, dst, n, (cudaStream_t)stream);
   return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "cast: %s", cudaGetErrorString(e));
 }
@@ -1804,6 +1822,7 @@ ppx_status ppx_bias_act(ppx_ctx* ctx, ppx_dtype dt, int32_t rows, int32_t cols, 
   if (!ctx) return PPX_E_CONFIG;
   if (rows < 1 || cols < 1 || !x || !y) return fail(ctx, PPX_E_CONFIG, "ppx_bias_act: bad arguments");
   lo_clear(ctx);
+  ++ctx->launches;
   cudaError_t e = ppx::launch_bias_act(dt == PPX_FP32, rows, cols, x, ldx, bias, act == PPX_RELU, y, ldy,
                                        (cudaStream_t)stream);
   return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "bias_act: %s", cudaGetErrorString(e));
@@ -1814,6 +1833,7 @@ ppx_status ppx_relu_mask(ppx_ctx* ctx, ppx_dtype dt, int32_t rows, int32_t cols,
   if (!ctx) return PPX_E_CONFIG;
   if (rows < 1 || cols < 1 || !x || !mask_src) return fail(ctx, PPX_E_CONFIG, "ppx_relu_mask: bad arguments");
   lo_clear(ctx);
+  ++ctx->launches;
   cudaError_t e = ppx::launch_relu_mask(dt == PPX_FP32, rows, cols, x, ldx, mask_src, ldm, (cudaStream_t)stream);
   return e == cudaSuccess ? PPX_OK : fail(ctx, PPX_E_CUDA, "relu_mask: %s", cudaGetErrorString(e));
 }

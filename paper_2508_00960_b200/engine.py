@@ -204,7 +204,6 @@ class PhantomEngine:
         if self.k3_fused:
             self.bwd_fused = False
         self._keep = []   # ctypes structs of the launch being built
-        self._launches = 0
         self.launch_count = 0
         self.trace = []   # kernel-launching ABI calls of the last step body (profiling labels)
         self._timing = None   # per-launch CUDA events (profile_step)
@@ -400,9 +399,10 @@ class PhantomEngine:
                      "ppx_backward_wgrad_errors"}
 
     def _call(self, name, *args, flops=0):
-        """ctx.call that counts the launches of our own kernels (NCCL / memsets excluded); under
-        profile_step() every kernel launch is bracketed by CUDA events on its stream and tagged
-        with its algorithmic GEMM FLOPs."""
+        """ctx.call that records the kernel-launching ABI calls of the step (`trace`, the labels
+        of ncu launch lists); under profile_step() every such call is bracketed by CUDA events on
+        its stream and tagged with its algorithmic GEMM FLOPs.  Kernel counts come from the
+        library itself (ppx_kernel_launches)."""
         timed = self._timing is not None and name in self._KERNEL_CALLS
         if timed:
             e0 = torch.cuda.Event(enable_timing=True)
@@ -413,7 +413,6 @@ class PhantomEngine:
             e1.record()
             self._timing.append((name, e0, e1, flops))
         if name in self._KERNEL_CALLS:
-            self._launches += 1
             self.trace.append(name)
 
     @staticmethod
@@ -629,8 +628,8 @@ class PhantomEngine:
 
     def _step_body(self, par, S):
         self._keep.clear()
-        self._launches = 0
         self.trace = []
+        k0 = self.ctx.kernel_launches
         st = S.cuda_stream
         nvtx = torch.cuda.nvtx
         nvtx.range_push(f"ppx.step[par={par}]")   # host-side NVTX ranges (ncu --nvtx / nsys filters)
@@ -648,7 +647,7 @@ class PhantomEngine:
         if self.world > 1:
             self._call("ppx_all_reduce_f32", self.loss.data_ptr(), 1, st)
         self._tf32_scope(0, st)
-        self.launch_count = self._launches
+        self.launch_count = self.ctx.kernel_launches - k0   # every kernel the step enqueued
         nvtx.range_pop()
 
     def _tf32_scope(self, on, st):
@@ -738,12 +737,12 @@ class PhantomEngine:
             self.infer_graphs[par].replay()
         else:
             self._keep.clear()
-            self._launches = 0
             st = torch.cuda.current_stream()
+            k0 = self.ctx.kernel_launches
             self._tf32_scope(1, st.cuda_stream)
             self._forward(par, st, train=False)
             self._tf32_scope(0, st.cuda_stream)
-            self.infer_launch_count = self._launches
+            self.infer_launch_count = self.ctx.kernel_launches - k0
         return [self.Y[par][jj][self.L] for jj in range(self.R)]
 
     def capture_inference(self):
@@ -755,12 +754,12 @@ class PhantomEngine:
             cs.wait_stream(torch.cuda.current_stream())
             with torch.cuda.graph(g, stream=cs):
                 self._keep.clear()
-                self._launches = 0
                 st = torch.cuda.current_stream()
+                k0 = self.ctx.kernel_launches
                 self._tf32_scope(1, st.cuda_stream)
                 self._forward(par, st, train=False)
                 self._tf32_scope(0, st.cuda_stream)
-                self.infer_launch_count = self._launches
+                self.infer_launch_count = self.ctx.kernel_launches - k0
             self.infer_graphs[par] = g
         torch.cuda.synchronize()
 

@@ -260,19 +260,17 @@ class TPEngine:
         epi = _lib.Epilogue(act, bias, 0, mask, ld_mask, colsum)
         self._keep.append(epi)
         self.ctx.call("ppx_gemm", self.pdt, M, N, K, a, lda, ta, b, ldb, tb, c, ldc, self.pdt, ctypes.byref(epi), st)
-        self._launches += 1
 
     def _gemm_update(self, M, N, K, a, lda, ta, b, ldb, tb, master, w_next, ld_w, st):
         u = _lib.Update(_lib.PPX_UPDATE_SGD, self.hyper.data_ptr(), master, w_next, None, None, None,
                         self.bad.data_ptr())
         self._keep.append(u)
         self.ctx.call("ppx_gemm_update", self.pdt, M, N, K, a, lda, ta, b, ldb, tb, ctypes.byref(u), ld_w, st)
-        self._launches += 1
 
     def _step_body(self, par, S):
         self._keep.clear()
-        self._launches = 0
         c, st = self.ctx, S.cuda_stream
+        k0 = c.kernel_launches
         n, s, B, P, pdt = self.n, self.s, self.B, self.P, self.pdt
         X, Ya = self.X[par], self.Ya
         c.call("ppx_zero", self.loss.data_ptr(), 4, st)
@@ -285,18 +283,15 @@ class TPEngine:
             c.call("ppx_all_reduce", pdt, X[m + 1].data_ptr(), B * n, st)
             c.call("ppx_bias_act", pdt, B, n, X[m + 1].data_ptr(), n, self._bb(m).data_ptr(), _lib.PPX_RELU,
                    X[m + 1].data_ptr(), n, st)
-            self._launches += 1
         mean = self.reduction == "mean"
         cur = 0
         c.call("ppx_output_delta", pdt, B, n, _lib.PPX_RELU, X[P].data_ptr(), n, self.Tgt[par].data_ptr(), n,
                X[P].data_ptr(), n, self.Dfull[cur].data_ptr(), n, 1.0 / B if mean else 1.0,
                0.5 / B if mean else 0.5, self.loss.data_ptr(), st)
-        self._launches += 1
         # ---- backward
         for m in range(P - 1, -1, -1):
             D = self.Dfull[cur]
             c.call("ppx_colsum", pdt, B, n, D.data_ptr(), n, self._gbb(m).data_ptr(), 0, st)
-            self._launches += 1
             # d Wb = D^T Ya  [n, s]  (+SGD)
             self._gemm_update(n, s, B, D.data_ptr(), n, 1, Ya[m].data_ptr(), s, 0, self.Wb[m].data_ptr(),
                               self.wb[1 - par][m].data_ptr(), s, st)
@@ -312,12 +307,10 @@ class TPEngine:
                            st)
                 c.call("ppx_all_reduce", pdt, Dn.data_ptr(), B * n, st)
                 c.call("ppx_relu_mask", pdt, B, n, Dn.data_ptr(), n, X[m].data_ptr(), n, st)
-                self._launches += 1
                 cur = 1 - cur
         c.call("ppx_optimizer_step", _lib.PPX_UPDATE_SGD, self.hyper.data_ptr(), self.bias.data_ptr(),
                self.gbias.data_ptr(), None, None, self.bias.numel(), _lib.PPX_FP32, None, self.bad.data_ptr(), st)
-        self._launches += 1
-        self.launch_count = self._launches
+        self.launch_count = c.kernel_launches - k0   # kernels enqueued by this step (GEMMs + helpers)
 
     def step(self, graph: bool = True):
         par = self.parity
