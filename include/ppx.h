@@ -291,6 +291,15 @@ typedef struct {
                                (the engine all-gathers each half separately to overlap it) */
 } ppx_wgrad_item;
 ppx_status ppx_wgrad(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad_item* items, void* stream);
+/* phantom.py:247-249 — compressor gradients only (parts == PPX_GRAD_COMP, p > 1) with the batch
+   (K) split into nsplit chunks: grouped launches of nitems x nsplit problems store fp32 partial
+   sums in partials[item][chunk][k, lds] (caller's buffer, nitems * nsplit * k * lds floats, padding
+   columns zero), then one elementwise pass per item sums the chunks in chunk order (deterministic)
+   and applies upd (SGD / Adam, w_next copy, upd->grad) or stores the raw gradient to grad.  The
+   engine uses it for the layer-0 compressor gradient: k x s over K = B is only a few long tiles,
+   the step's exposed tail. */
+ppx_status ppx_wgrad_splitk(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad_item* items,
+                            int32_t nsplit, float* partials, void* stream);
 
 /* phantom.py:199-207 + 239-267 in ONE LPT-scheduled launch of the 2-SM kernel (bf16): the error
    compression of the n local ranks io[] (as ppx_error_phantoms_n, into contrib [p][B, ldk]; with

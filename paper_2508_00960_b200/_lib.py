@@ -116,6 +116,7 @@ _SIGS = {
     "ppx_param_grads": (_i32, [_vp, _i32, ctypes.POINTER(Layer), _i32, _vp, _i64, _vp, _i64, _vp,
                                _vp, _fp, ctypes.POINTER(Update), _i32, _vp]),
     "ppx_wgrad": (_i32, [_vp, _i32, _i32, ctypes.POINTER(WgradItem), _vp]),
+    "ppx_wgrad_splitk": (_i32, [_vp, _i32, _i32, ctypes.POINTER(WgradItem), _i32, _fp, _vp]),
     "ppx_backward_delta": (_i32, [_vp, _i32, ctypes.POINTER(Layer), _i32, _i32, _vp, _i64, _vp,
                                   _vp, _i64, _vp, _i64, _fp, _vp]),
     "ppx_colsum": (_i32, [_vp, _i32, _i32, _i32, _vp, _i64, _fp, _i32, _vp]),

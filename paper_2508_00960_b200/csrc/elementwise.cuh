@@ -131,25 +131,28 @@ inline cudaError_t launch_colsum(bool f32, int rows, int cols, const void* x, in
 
 // ---- SGD / Adam (training.py:74-82, 92-105) with non-finite detection -------------------------
 // hyper = [lr, beta1, beta2, eps, 1 - beta1^t, 1 - beta2^t]
+__device__ __forceinline__ float opt_apply(bool adam, const float* __restrict__ hyper, float gi, float wi,
+                                           float* __restrict__ m, float* __restrict__ v, int64_t i) {
+  const float lr = hyper[0];
+  if (adam) {
+    const float b1 = hyper[1], b2 = hyper[2], eps = hyper[3], bc1 = hyper[4], bc2 = hyper[5];
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    return wi - lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+  }
+  return wi - lr * gi;
+}
+
 __global__ void optimizer_kernel(bool adam, const float* __restrict__ hyper, float* __restrict__ w,
                                  const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v, int64_t n,
                                  bool copy_f32, void* copy, int* bad) {
-  const float lr = hyper[0];
   bool nonfinite = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float gi = g[i];
     nonfinite |= !isfinite(gi);
-    float wi = w[i];
-    if (adam) {
-      const float b1 = hyper[1], b2 = hyper[2], eps = hyper[3], bc1 = hyper[4], bc2 = hyper[5];
-      const float mi = b1 * m[i] + (1.f - b1) * gi;
-      const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
-      m[i] = mi;
-      v[i] = vi;
-      wi -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
-    } else {
-      wi -= lr * gi;
-    }
+    const float wi = opt_apply(adam, hyper, gi, w[i], m, v, i);
     w[i] = wi;
     if (copy) st_elem(copy, i, copy_f32, wi);
   }
@@ -158,6 +161,35 @@ __global__ void optimizer_kernel(bool adam, const float* __restrict__ hyper, flo
 inline cudaError_t launch_optimizer(bool adam, const float* hyper, float* w, const float* g, float* m, float* v,
                                     int64_t n, bool copy_f32, void* copy, int* bad, cudaStream_t st) {
   optimizer_kernel<<<ew_grid(n), 256, 0, st>>>(adam, hyper, w, g, m, v, n, copy_f32, copy, bad);
+  return cudaGetLastError();
+}
+
+// Split-K weight gradient, second half: g = sum of `nparts` fp32 partial sums (in chunk order, so
+// deterministic), optionally stored to g_out, then SGD / Adam (mode 1 / 2; 0 = none) on w with the
+// new weights also written to `copy` in the compute dtype
+__global__ void splitk_update_kernel(int mode, const float* __restrict__ hyper, const float* __restrict__ parts,
+                                     int nparts, int64_t part_stride, int64_t n, float* __restrict__ w,
+                                     float* __restrict__ m, float* __restrict__ v, bool copy_f32, void* copy,
+                                     float* __restrict__ g_out, int* bad) {
+  bool nonfinite = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float gi = 0.f;
+    for (int c = 0; c < nparts; ++c) gi += __ldg(parts + c * part_stride + i);
+    nonfinite |= !isfinite(gi);
+    if (g_out) g_out[i] = gi;
+    if (mode) {
+      const float wi = opt_apply(mode == 2, hyper, gi, w[i], m, v, i);
+      w[i] = wi;
+      if (copy) st_elem(copy, i, copy_f32, wi);
+    }
+  }
+  if (bad && __any_sync(0xffffffffu, nonfinite) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+}
+inline cudaError_t launch_splitk_update(int mode, const float* hyper, const float* parts, int nparts,
+                                        int64_t part_stride, int64_t n, float* w, float* m, float* v, bool copy_f32,
+                                        void* copy, float* g_out, int* bad, cudaStream_t st) {
+  splitk_update_kernel<<<ew_grid(n), 256, 0, st>>>(mode, hyper, parts, nparts, part_stride, n, w, m, v, copy_f32,
+                                                   copy, g_out, bad);
   return cudaGetLastError();
 }
 

@@ -1556,6 +1556,75 @@ ppx_status ppx_wgrad(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad
   return PPX_OK;
 }
 
+// Compressor gradients with the batch (K) split into nsplit chunks (phantom.py:247-249, the
+// layer-0 compressor gradient: the step's exposed tail, k rows x s columns over K = B is a handful
+// of long tiles): grouped launches of nitems x nsplit problems storing fp32 partial sums into
+// partials[item][chunk][k, lds], then per item ONE elementwise pass that sums the chunks in order
+// and applies the fused update (and/or stores the raw gradient).
+ppx_status ppx_wgrad_splitk(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad_item* items, int32_t nsplit,
+                            float* partials, void* stream) {
+  if (!ctx) return PPX_E_CONFIG;
+  if (nitems < 1 || !items || nsplit < 1 || nsplit > ppx::MAX_PROBS || !partials)
+    return fail(ctx, PPX_E_CONFIG, "ppx_wgrad_splitk: bad arguments");
+  for (int i = 0; i < nitems; ++i) {
+    const ppx_wgrad_item& it = items[i];
+    const ppx_layer* L = it.layer;
+    const bool update = it.upd && it.upd->kind != PPX_UPDATE_NONE;
+    if (bad_layer(L) || it.parts != PPX_GRAD_COMP || L->p < 2 || !it.received || !it.y_prev || it.B < nsplit ||
+        it.B % nsplit || (!it.grad && !update))
+      return fail(ctx, PPX_E_CONFIG, "ppx_wgrad_splitk: compressor gradients (p > 1) with B %% nsplit == 0 only");
+    if (update && (!it.upd->master || !it.upd->hyper ||
+                   (it.upd->kind == PPX_UPDATE_ADAM && (!it.upd->adam_m || !it.upd->adam_v))))
+      return fail(ctx, PPX_E_CONFIG, "ppx_wgrad_splitk: incomplete update");
+  }
+  const cudaStream_t st = (cudaStream_t)stream;
+  int q = 0;
+  const int total = nitems * nsplit;
+  while (q < total) {
+    Builder b(ctx, dt, stream);
+    for (; q < total && b.P.nprobs < ppx::MAX_PROBS; ++q) {
+      const ppx_wgrad_item& it = items[q / nsplit];
+      const int c = q % nsplit;
+      const ppx_layer* L = it.layer;
+      Flat f(L->s, L->k, L->p);
+      const int Bc = it.B / nsplit;
+      Problem* pr = b.new_problem(L->k, L->s, 1, true);
+      // the chunks as slots of one view per operand: every chunk problem shares its tensor maps
+      Opnd r{view3(it.received, nsplit, Bc, L->k, f.ldk, (int64_t)Bc * f.ldk)};
+      r.mn = 1;
+      r.slot_base = c;
+      Opnd y{view3(it.y_prev, nsplit, Bc, L->s, it.ld_y, (int64_t)Bc * it.ld_y)};
+      y.mn = 1;
+      y.slot_base = c;
+      const int kt = (int)cdiv(Bc, b.BK);
+      b.add_segment(pr, r, y, kt, kt);
+      if (pr) pr->epi.out = t2(partials + (int64_t)q * L->k * f.lds, f.lds, 1);
+    }
+    ppx_status s = b.launch();
+    if (s != PPX_OK) return s;
+  }
+  for (int i = 0; i < nitems; ++i) {
+    const ppx_wgrad_item& it = items[i];
+    const ppx_layer* L = it.layer;
+    const ppx_update* u = it.upd;
+    const bool update = u && u->kind != PPX_UPDATE_NONE;
+    Flat f(L->s, L->k, L->p);
+    const int64_t n = (int64_t)L->k * f.lds;
+    float* w = update ? u->master + f.comp : nullptr;
+    lo_invalidate(ctx, w, n * 4);
+    if (update && u->w_next) lo_invalidate(ctx, elem(dt, u->w_next, f.comp), n * (dt == PPX_FP32 ? 4 : 2));
+    ++ctx->launches;
+    cudaError_t e = ppx::launch_splitk_update(
+        update ? (u->kind == PPX_UPDATE_ADAM ? 2 : 1) : 0, update ? u->hyper : nullptr, partials + (int64_t)i * nsplit * n,
+        nsplit, n, n, w, update && u->adam_m ? u->adam_m + f.comp : nullptr,
+        update && u->adam_v ? u->adam_v + f.comp : nullptr, dt == PPX_FP32,
+        update && u->w_next ? (char*)u->w_next + f.comp * (dt == PPX_FP32 ? 4 : 2) : nullptr,
+        update ? (u->grad ? u->grad + f.comp : nullptr) : it.grad + f.comp, update ? u->bad : nullptr, st);
+    if (e != cudaSuccess) return fail(ctx, PPX_E_CUDA, "splitk update: %s", cudaGetErrorString(e));
+  }
+  return PPX_OK;
+}
+
 static ppx_status add_backward(ppx_ctx* ctx, ppx_dtype dt, Builder& b, const ppx_rank_io& io, int32_t B,
                                ppx_act act_prev) {
   const ppx_layer* L = io.layer;

@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import torch
 
@@ -203,6 +204,11 @@ class PhantomEngine:
         self.k3_fused = (k3_ok and self.group <= 2) if k3_fused is None else bool(k3_fused)
         if self.k3_fused:
             self.bwd_fused = False
+        # layer-0 compressor gradient with the batch split (ppx_wgrad_splitk): fp32 partial sums
+        # (PPX_NO_SPLITK=1 keeps the one-launch form, A/B only)
+        self.splitk_off = bool(os.environ.get("PPX_NO_SPLITK"))
+        nparts = max((c1 - c0) * self._layer0_split(c1 - c0) for c0, c1 in self._chunks()) if p > 1 else 0
+        self.splitk_parts = torch.zeros(max(1, nparts * k * self.off["lds"]), dtype=f32, device=self.dev)
         self._keep = []   # ctypes structs of the launch being built
         self.launch_count = 0
         self.trace = []   # kernel-launching ABI calls of the last step body (profiling labels)
@@ -396,7 +402,7 @@ class PhantomEngine:
                      "ppx_backward_delta", "ppx_optimizer_step", "ppx_compress_n", "ppx_forward_n",
                      "ppx_error_phantoms_n", "ppx_forward_fused", "ppx_error_phantoms_scatter", "ppx_reduce_received",
                      "ppx_backward_fused", "ppx_backward_delta_n", "ppx_hyper_advance",
-                     "ppx_backward_wgrad_errors"}
+                     "ppx_backward_wgrad_errors", "ppx_wgrad_splitk"}
 
     def _call(self, name, *args, flops=0):
         """ctx.call that records the kernel-launching ABI calls of the step (`trace`, the labels
@@ -492,6 +498,19 @@ class PhantomEngine:
             f += 2 * B * s * (p - 1) * k if it.parts & _lib.GRAD_DEC else 0
             f += 2 * B * s * k if it.parts & _lib.GRAD_COMP else 0
         return f
+
+    def _layer0_split(self, n_items):
+        """Batch chunks of the layer-0 compressor gradient (ppx_wgrad_splitk): doubled while the
+        launch would leave most SMs idle (< 74 tiles of the 2-SM kernel) and the chunks stay
+        whole 128-row K blocks, at most 16 problems per launch; 1 = unsplit."""
+        if self.splitk_off:
+            return 1
+        tiles = n_items * -(-self.k // 256) * -(-self.s // 256)
+        nsplit = 1
+        while (tiles * nsplit < 74 and n_items * nsplit * 2 <= 16 and self.B % (nsplit * 2) == 0
+               and (self.B // (nsplit * 2)) % 128 == 0):
+            nsplit *= 2
+        return nsplit
 
     def _launch_wgrad(self, items, st):
         arr = (_lib.WgradItem * len(items))(*items)
@@ -618,7 +637,14 @@ class PhantomEngine:
                  for jj in range(R)]
         if self.p > 1:
             for c0, c1 in self._chunks():
-                self._launch_wgrad(items[c0:c1], st)
+                nsplit = self._layer0_split(c1 - c0)
+                if nsplit > 1:   # a few long k x s tiles over K = B: split the batch, sum + update after
+                    arr = (_lib.WgradItem * (c1 - c0))(*items[c0:c1])
+                    self._keep.append(arr)
+                    self._call("ppx_wgrad_splitk", pdt, c1 - c0, arr, nsplit, self.splitk_parts.data_ptr(), st,
+                               flops=sum(self._f_item(it) for it in items[c0:c1]))
+                else:
+                    self._launch_wgrad(items[c0:c1], st)
         # biases of all local ranks and layers in one elementwise launch
         kind = _lib.PPX_UPDATE_ADAM if self.optimizer == "adam" else _lib.PPX_UPDATE_SGD
         self._call("ppx_optimizer_step", kind, self.hyper.data_ptr(), self.bias.data_ptr(), self.gbias.data_ptr(),

@@ -103,6 +103,31 @@ def test_engine_steps_match_oracle(dtype, tol, optimizer, graph):
     _check_updates(eng, model0, model, tol if dtype == torch.float32 else (1e-1 if optimizer == "sgd" else 2.5e-1))
 
 
+@pytest.mark.parametrize("optimizer", ["sgd", "adam"])
+@pytest.mark.parametrize("group", [None, 1])
+def test_engine_layer0_splitk_matches_oracle(optimizer, group):
+    """B = 512 splits the layer-0 compressor gradient over the batch (ppx_wgrad_splitk: 4 chunks
+    of fp32 partial sums, then the summing SGD / Adam pass): fp32 tier vs the oracle over 3 graph
+    steps, and the plan really took the split.  SGD 1e-4; Adam 1e-3: at this shape Adam's
+    m / sqrt(v) turns the fp32 rounding of near-zero gradient entries into up to 6.8e-4 normwise
+    update error in the layer-0 tensors — identical with the split off (PPX_NO_SPLITK=1), so it
+    is the tier's arithmetic, not the split."""
+    n, p, k, L, B = 512, 4, 32, 2, 512
+    lr = 3e-3 if optimizer == "sgd" else 1e-3
+    eng, model, x, y = _setup(n, p, k, L, B, torch.float32, optimizer, lr, group=group)
+    assert eng._layer0_split(eng.group) > 1
+    model0 = copy.deepcopy(model)
+    eng.step(graph=False)
+    assert "ppx_wgrad_splitk" in eng.trace
+    eng.capture()
+    for _ in range(2):
+        eng.step()
+    loss = eng.read_loss()
+    ref = _oracle_steps(model, x, y, L, 3, optimizer, lr)
+    assert abs(loss - ref[-1]) <= 1e-4 * abs(ref[-1]), (loss, ref)
+    _check_updates(eng, model0, model, 1e-4 if optimizer == "sgd" else 1e-3)
+
+
 @pytest.mark.parametrize("optimizer", ["adam", "sgd"])
 def test_engine_unsynchronised_graph_replays(optimizer):
     """Five CUDA-graph steps issued back to back with no host synchronisation in between (the

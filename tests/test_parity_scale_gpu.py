@@ -74,6 +74,7 @@ def _step_and_check(eng, ts, steps=2, sensitivity=True):
     (512, 4, 64, 3, 256, {"group": 1, "k3_fused": False}),  # per-rank, [wgrad + recurrence] fused
     (768, 4, 24, 2, 96, {"fused": False}),   # ragged k / batch tiles
     (512, 4, 64, 3, 256, {"mask_bits": False}),   # ReLU' mask from the bf16 activations
+    (512, 4, 64, 2, 512, {"group": 1}),  # layer-0 compressor gradient split over the batch
 ])
 def test_small_shapes_teacher_forced(n, p, k, L, B, kw):
     """The small engine-test shapes, checked kernel by kernel (what the float64 step comparisons

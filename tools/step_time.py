@@ -11,6 +11,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
 ap.add_argument("--steps", type=int, default=40)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--group", type=int, default=0, help="logical ranks per launch (1 = the 8-GPU per-GPU shapes)")
 a = ap.parse_args()
 cfg = bench.CONFIGS[a.config]
 world, rank, local = int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0))
@@ -19,7 +20,7 @@ if world > 1:
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 D = bench.Dist(world, rank, local)
 eng = PhantomEngine(cfg["n"], cfg["p"], cfg["k"], cfg["layers"], cfg["batch"], world=world, rank=rank, device=local,
-                    uid=D.uid(), lr=3e-6)
+                    uid=D.uid(), lr=3e-6, group=a.group or None)
 xs, ts = bench.make_data(eng, 1234, cfg)
 eng.set_batch(xs, ts, 0)
 eng.set_batch(xs, ts, 1)
@@ -29,7 +30,8 @@ for _ in range(5):
     eng.step()
 ms = [bench.timed_steps(eng, D, a.steps) for _ in range(a.reps)]
 if rank == 0:
-    print(json.dumps({"config": a.config, "world": world, "env": os.environ.get("PPX_DEBUG_EPI", ""), "ms": ms}))
+    env = {k: v for k, v in os.environ.items() if k.startswith(("PPX_DEBUG", "PPX_NO_", "PPX_AB_"))}
+    print(json.dumps({"config": a.config, "world": world, "group": eng.group, "env": env, "ms": ms}))
 D.barrier()
 eng.close()
 bench.finish(D)
