@@ -17,11 +17,14 @@ max over ranks.  The same JSON line also carries:
               per launch from the committed ncu capture (profiles/traffic.json, commit-stamped)
   r1_shapes   (N=1) the same step with one logical rank per launch: the per-GPU kernels of the
               8-GPU run, so every 1-GPU bench records their efficiency
+  fp32_tier   (N=1) the fp32 parity tier (3xTF32) at C2: samples/s and fraction of that tier's
+              tensor ceiling (bf16 peak / 6)
   inference   (C3/C5) forward-only samples/s of the same model (config C5 at k = 128)
   energy      NVML joules per epoch (64 batches) over >= --energy-seconds of steady-state steps
   tp          the same-width Megatron tensor-parallel pipeline on the same GPUs (its energy too)
-  e2e         the public API with pinned HOST batches: H2D of inputs+targets and D2H of the loss
-              inside the timed region
+  e2e         the public API with pinned HOST batches: H2D of inputs+targets and D2H of every
+              step's loss inside the timed region (the host reads step i's loss while step i+1
+              runs, Engine.loss_async)
   cpu_baseline  the reference algorithm on this box's host cores (bounded sample)
 
 --config c5 runs the inference sweep (k = 32..512) instead of training.  --impl reference times
@@ -410,6 +413,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tp", action="store_true")
     ap.add_argument("--no-r1", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true")
     args = ap.parse_args()
     refuse_debug_knobs()
     cfg = dict(CONFIGS[args.config])
@@ -506,6 +510,15 @@ def main():
         r1 = time_r1_shapes(cfg, D, xs, ts, args, peak, peak_sus)
         eng = None
 
+    fp32_tier = None
+    if world == 1 and args.config == "c3" and args.dtype == "bf16" and not args.no_fp32:
+        if eng is not None:
+            eng.close()
+            del eng
+            eng = None
+            torch.cuda.empty_cache()
+        fp32_tier = time_fp32_tier(D, args, peak)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args, cfg)
@@ -541,6 +554,7 @@ def main():
             "loss": {"after_warmup": loss0, "after_timed": loss1},
             "comm_bytes_per_step_per_gpu": comm_bytes_per_step(n, p, k, L, B, world),
             "r1_shapes": r1,
+            "fp32_tier": fp32_tier,
             "inference": inference,
             "tp": tp,
         }
@@ -698,6 +712,31 @@ def time_r1_shapes(cfg, D, xs, ts, args, peak, peak_sus):
             "kernel_sum_frac_of_burst": flops / (kern_ms / 1e3) / 1e12 / peak,
             "kernel_sum_frac_of_sustained": flops / (kern_ms / 1e3) / 1e12 / peak_sus,
             "launches_per_step": eng.launch_count, "kernels": kernels}
+
+
+def time_fp32_tier(D, args, peak):
+    """The fp32 parity tier (3xTF32 on kind::tf32, the tier that carries the 1e-4 oracle parity)
+    at C2 on this GPU: graph-replayed training steps of the default plan."""
+    import torch
+    from paper_2508_00960_b200.engine import PhantomEngine, pp_step_flops
+    cfg = CONFIGS["c2"]
+    n, p, k, L, B = cfg["n"], cfg["p"], cfg["k"], cfg["layers"], cfg["batch"]
+    eng = PhantomEngine(n, p, k, L, B, lr=3e-6, dtype=torch.float32)
+    xs, ts = make_data(eng, 1234, cfg)
+    eng.set_batch(xs, ts, 0)
+    eng.set_batch(xs, ts, 1)
+    eng.step(graph=False)
+    launches = eng.launch_count
+    eng.capture()
+    for _ in range(3):
+        eng.step()
+    ms = timed_steps(eng, D, max(5, min(args.steps, 10)))
+    eng.close()
+    tf = eng.R * pp_step_flops(n, p, k, L, B) / (ms / 1e3) / 1e12
+    return {"what": "C2 (n=8192, L=8, p=4, k=64, batch 8192) in the fp32 tier (3xTF32), 1 GPU",
+            "samples_per_s": B / (ms / 1e3), "ms_per_step": ms, "step_tflops": tf,
+            "frac_of_tier_ceiling": 6 * tf / peak, "launches_per_step": launches,
+            "tier_note": "three kind::tf32 MMAs per product at half the bf16 rate: ceiling = bf16 peak / 6"}
 
 
 def run_tp(args, cfg, D, eng, uid):

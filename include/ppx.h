@@ -294,8 +294,9 @@ ppx_status ppx_wgrad(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad
 /* phantom.py:247-249 — compressor gradients only (parts == PPX_GRAD_COMP, p > 1) with the batch
    (K) split into nsplit chunks: grouped launches of nitems x nsplit problems store fp32 partial
    sums in partials[item][chunk][k, lds] (caller's buffer, nitems * nsplit * k * lds floats, padding
-   columns zero), then one elementwise pass per item sums the chunks in chunk order (deterministic)
-   and applies upd (SGD / Adam, w_next copy, upd->grad) or stores the raw gradient to grad.  The
+   columns zero), then ONE elementwise launch sums each item's chunks in chunk order
+   (deterministic) and applies upd (SGD / Adam, w_next copy, upd->grad) or stores the raw gradient
+   to grad.  1..16 items sharing (s, k, p) and the update kind / hyper / bad flag.  The
    engine uses it for the layer-0 compressor gradient: k x s over K = B is only a few long tiles,
    the step's exposed tail. */
 ppx_status ppx_wgrad_splitk(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad_item* items,

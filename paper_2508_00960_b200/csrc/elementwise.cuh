@@ -164,21 +164,41 @@ inline cudaError_t launch_optimizer(bool adam, const float* hyper, float* w, con
   return cudaGetLastError();
 }
 
-// Split-K weight gradient, second half: g = sum of `nparts` fp32 partial sums (in chunk order, so
-// deterministic), optionally stored to g_out, then SGD / Adam (mode 1 / 2; 0 = none) on w with the
-// new weights also written to `copy` in the compute dtype
+// Split-K weight gradient, second half, for up to 16 items (blockIdx.y): g = sum of `nparts` fp32
+// partial sums (in chunk order, so deterministic), optionally stored to g_out, then SGD / Adam
+// (mode 1 / 2; 0 = none) on w with the new weights also written to `copy` in the compute dtype
+struct SplitkItems {
+  float* w[16];
+  float* m[16];
+  float* v[16];
+  void* copy[16];
+  float* g_out[16];
+};
 __global__ void splitk_update_kernel(int mode, const float* __restrict__ hyper, const float* __restrict__ parts,
-                                     int nparts, int64_t part_stride, int64_t n, float* __restrict__ w,
-                                     float* __restrict__ m, float* __restrict__ v, bool copy_f32, void* copy,
-                                     float* __restrict__ g_out, int* bad) {
+                                     int nparts, int64_t part_stride, int64_t n, const __grid_constant__ SplitkItems it,
+                                     bool copy_f32, int* bad) {
+  const int q = blockIdx.y;
+  const float* pq = parts + (int64_t)q * nparts * part_stride;
+  float* w = it.w[q];
+  float* g_out = it.g_out[q];
+  void* copy = it.copy[q];
   bool nonfinite = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    // eight loads in flight per thread, summed in chunk order
     float gi = 0.f;
-    for (int c = 0; c < nparts; ++c) gi += __ldg(parts + c * part_stride + i);
+    int c = 0;
+    for (; c + 8 <= nparts; c += 8) {
+      float a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = __ldg(pq + (c + u) * part_stride + i);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) gi += a[u];
+    }
+    for (; c < nparts; ++c) gi += __ldg(pq + c * part_stride + i);
     nonfinite |= !isfinite(gi);
     if (g_out) g_out[i] = gi;
     if (mode) {
-      const float wi = opt_apply(mode == 2, hyper, gi, w[i], m, v, i);
+      const float wi = opt_apply(mode == 2, hyper, gi, w[i], it.m[q], it.v[q], i);
       w[i] = wi;
       if (copy) st_elem(copy, i, copy_f32, wi);
     }
@@ -186,10 +206,13 @@ __global__ void splitk_update_kernel(int mode, const float* __restrict__ hyper, 
   if (bad && __any_sync(0xffffffffu, nonfinite) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
 }
 inline cudaError_t launch_splitk_update(int mode, const float* hyper, const float* parts, int nparts,
-                                        int64_t part_stride, int64_t n, float* w, float* m, float* v, bool copy_f32,
-                                        void* copy, float* g_out, int* bad, cudaStream_t st) {
-  splitk_update_kernel<<<ew_grid(n), 256, 0, st>>>(mode, hyper, parts, nparts, part_stride, n, w, m, v, copy_f32,
-                                                   copy, g_out, bad);
+                                        int64_t part_stride, int64_t n, int nitems, const SplitkItems& it,
+                                        bool copy_f32, int* bad, cudaStream_t st) {
+  int gx = ew_grid(n);
+  const int cap = 148 * 16 / nitems;
+  gx = gx > cap ? (cap < 1 ? 1 : cap) : gx;
+  splitk_update_kernel<<<dim3(gx, nitems), 256, 0, st>>>(mode, hyper, parts, nparts, part_stride, n, it, copy_f32,
+                                                         bad);
   return cudaGetLastError();
 }
 

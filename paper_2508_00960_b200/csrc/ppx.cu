@@ -1564,8 +1564,8 @@ ppx_status ppx_wgrad(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad
 ppx_status ppx_wgrad_splitk(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const ppx_wgrad_item* items, int32_t nsplit,
                             float* partials, void* stream) {
   if (!ctx) return PPX_E_CONFIG;
-  if (nitems < 1 || !items || nsplit < 1 || nsplit > ppx::MAX_PROBS || !partials)
-    return fail(ctx, PPX_E_CONFIG, "ppx_wgrad_splitk: bad arguments");
+  if (nitems < 1 || nitems > 16 || !items || nsplit < 1 || nsplit > ppx::MAX_PROBS || !partials)
+    return fail(ctx, PPX_E_CONFIG, "ppx_wgrad_splitk: bad arguments (1..16 items)");
   for (int i = 0; i < nitems; ++i) {
     const ppx_wgrad_item& it = items[i];
     const ppx_layer* L = it.layer;
@@ -1580,8 +1580,13 @@ ppx_status ppx_wgrad_splitk(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const pp
   const cudaStream_t st = (cudaStream_t)stream;
   int q = 0;
   const int total = nitems * nsplit;
+  int kmax = 0;
+  for (int i = 0; i < nitems; ++i) kmax = items[i].layer->k > kmax ? items[i].layer->k : kmax;
   while (q < total) {
     Builder b(ctx, dt, stream);
+    // k <= 128 rows fit the 1-SM kernel's tile exactly: a 2-SM pair tile would leave its second
+    // CTA's 128 rows empty, and 148 single SMs take the chunk tiles in one round
+    if (kmax <= ppx::BM) b.want_pair = false;
     for (; q < total && b.P.nprobs < ppx::MAX_PROBS; ++q) {
       const ppx_wgrad_item& it = items[q / nsplit];
       const int c = q % nsplit;
@@ -1603,25 +1608,38 @@ ppx_status ppx_wgrad_splitk(ppx_ctx* ctx, ppx_dtype dt, int32_t nitems, const pp
     ppx_status s = b.launch();
     if (s != PPX_OK) return s;
   }
+  // one summing + update launch for all items (they share k, s, the update kind and hyper)
+  const ppx_wgrad_item& i0 = items[0];
+  const bool update = i0.upd && i0.upd->kind != PPX_UPDATE_NONE;
+  const int mode = update ? (i0.upd->kind == PPX_UPDATE_ADAM ? 2 : 1) : 0;
+  Flat f0(i0.layer->s, i0.layer->k, i0.layer->p);
+  const int64_t n = (int64_t)i0.layer->k * f0.lds;
+  const int es = dt == PPX_FP32 ? 4 : 2;
+  ppx::SplitkItems si;
+  memset(&si, 0, sizeof(si));
   for (int i = 0; i < nitems; ++i) {
     const ppx_wgrad_item& it = items[i];
-    const ppx_layer* L = it.layer;
     const ppx_update* u = it.upd;
-    const bool update = u && u->kind != PPX_UPDATE_NONE;
-    Flat f(L->s, L->k, L->p);
-    const int64_t n = (int64_t)L->k * f.lds;
-    float* w = update ? u->master + f.comp : nullptr;
-    lo_invalidate(ctx, w, n * 4);
-    if (update && u->w_next) lo_invalidate(ctx, elem(dt, u->w_next, f.comp), n * (dt == PPX_FP32 ? 4 : 2));
-    ++ctx->launches;
-    cudaError_t e = ppx::launch_splitk_update(
-        update ? (u->kind == PPX_UPDATE_ADAM ? 2 : 1) : 0, update ? u->hyper : nullptr, partials + (int64_t)i * nsplit * n,
-        nsplit, n, n, w, update && u->adam_m ? u->adam_m + f.comp : nullptr,
-        update && u->adam_v ? u->adam_v + f.comp : nullptr, dt == PPX_FP32,
-        update && u->w_next ? (char*)u->w_next + f.comp * (dt == PPX_FP32 ? 4 : 2) : nullptr,
-        update ? (u->grad ? u->grad + f.comp : nullptr) : it.grad + f.comp, update ? u->bad : nullptr, st);
-    if (e != cudaSuccess) return fail(ctx, PPX_E_CUDA, "splitk update: %s", cudaGetErrorString(e));
+    const bool upd_i = u && u->kind != PPX_UPDATE_NONE;
+    if (upd_i != update || (update && (u->kind != i0.upd->kind || u->hyper != i0.upd->hyper || u->bad != i0.upd->bad)) ||
+        it.layer->k != i0.layer->k || it.layer->s != i0.layer->s || it.layer->p != i0.layer->p)
+      return fail(ctx, PPX_E_CONFIG, "ppx_wgrad_splitk: items must share the shapes and the update");
+    if (update) {
+      si.w[i] = u->master + f0.comp;
+      si.m[i] = u->adam_m ? u->adam_m + f0.comp : nullptr;
+      si.v[i] = u->adam_v ? u->adam_v + f0.comp : nullptr;
+      si.copy[i] = u->w_next ? (char*)u->w_next + f0.comp * es : nullptr;
+      si.g_out[i] = u->grad ? u->grad + f0.comp : nullptr;
+      lo_invalidate(ctx, si.w[i], n * 4);
+      if (si.copy[i]) lo_invalidate(ctx, si.copy[i], n * es);
+    } else {
+      si.g_out[i] = it.grad + f0.comp;
+    }
   }
+  ++ctx->launches;
+  cudaError_t e = ppx::launch_splitk_update(mode, update ? i0.upd->hyper : nullptr, partials, nsplit, n, n, nitems, si,
+                                            dt == PPX_FP32, update ? i0.upd->bad : nullptr, st);
+  if (e != cudaSuccess) return fail(ctx, PPX_E_CUDA, "splitk update: %s", cudaGetErrorString(e));
   return PPX_OK;
 }
 

@@ -500,14 +500,15 @@ class PhantomEngine:
         return f
 
     def _layer0_split(self, n_items):
-        """Batch chunks of the layer-0 compressor gradient (ppx_wgrad_splitk): doubled while the
-        launch would leave most SMs idle (< 74 tiles of the 2-SM kernel) and the chunks stay
-        whole 128-row K blocks, at most 16 problems per launch; 1 = unsplit."""
+        """Batch chunks of the layer-0 compressor gradient (ppx_wgrad_splitk, 128 x 256 tiles of
+        the 1-SM kernel for k <= 128): doubled while the doubled launch still fits one round on
+        the 148 SMs and the chunks stay whole 128-row K blocks, at most 16 problems per launch;
+        1 = unsplit."""
         if self.splitk_off:
             return 1
-        tiles = n_items * -(-self.k // 256) * -(-self.s // 256)
+        tiles = n_items * -(-self.k // 128) * -(-self.s // 256)
         nsplit = 1
-        while (tiles * nsplit < 74 and n_items * nsplit * 2 <= 16 and self.B % (nsplit * 2) == 0
+        while (tiles * nsplit * 2 <= 148 and n_items * nsplit * 2 <= 16 and self.B % (nsplit * 2) == 0
                and (self.B // (nsplit * 2)) % 128 == 0):
             nsplit *= 2
         return nsplit
