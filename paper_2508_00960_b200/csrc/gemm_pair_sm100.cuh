@@ -2,8 +2,8 @@
 //
 // A CTA pair (cluster of 2) owns a 256 x BN output tile: each CTA stages 128 rows of A and BN/2
 // rows of B; the leader issues M=256 tcgen05.mma into both CTAs' TMEM.  A stage carries
-// K = 128 (two 64-wide SWIZZLE_128B atoms), so one stage is 8 MMAs = 1024 tensor cycles per SM
-// between barrier round trips (the 1-SM kernel's 4 MMAs / 512 cycles leaves the tensor pipe
+// K = PBK (default 128: two 64-wide SWIZZLE_128B atoms, 3 stages), so one stage is 8 MMAs = 1024
+// tensor cycles per SM between barrier round trips (the 1-SM kernel's 4 MMAs / 512 cycles leaves the tensor pipe
 // ~25% idle on barrier/issue latency).  Double-buffered TMEM accumulators (2 x 256 columns) keep
 // the epilogue of tile i under the MMAs of tile i+1.  Problems, segments, slot-blocked K / N
 // coordinates and the epilogue are shared with gemm_sm100.cuh (same GemmParams).
@@ -12,10 +12,15 @@
 
 namespace ppx {
 
-constexpr int PBK = 128;                         // K elements per stage (2 atoms)
-constexpr int PSTAGES = 3;
-constexpr int PA_STAGE = BM * 2 * ROW_BYTES;     // 32 KB: [2 K-atoms][128 rows][128 B]
-constexpr int PB_STAGE = 128 * 2 * ROW_BYTES;    // 32 KB: [2 K-atoms][<=128 rows][128 B]
+#ifndef PPX_PBK
+#define PPX_PBK 128
+#endif
+constexpr int PBK = PPX_PBK;                     // K elements per stage (PKA 64-wide atoms)
+constexpr int PKA = PBK / 64;
+static_assert(PBK % 64 == 0 && PKA >= 1 && PKA <= 4, "stage K must be 1..4 whole atoms");
+constexpr int PA_STAGE = BM * PKA * ROW_BYTES;   // [PKA K-atoms][128 rows][128 B] (32 KB at K 128)
+constexpr int PB_STAGE = 128 * PKA * ROW_BYTES;  // [PKA K-atoms][<=128 rows][128 B]
+constexpr int PSTAGES = (192 * 1024) / (PA_STAGE + PB_STAGE);   // 192 KB of operand ring
 constexpr int PSMEM_BYTES = PSTAGES * (PA_STAGE + PB_STAGE) + 1024 + 256 + EPI_STAGE_BYTES;
 
 __device__ __forceinline__ void tma4_pair(const CUtensorMap* map, uint32_t bar, uint32_t dst, int c0, int c1, int c2,
@@ -51,9 +56,9 @@ __device__ __forceinline__ void commit_pair(uint32_t bar) {
 }
 
 // Operand maps for this kernel (host side, ppx.cu):
-//   K-major:          4D {64, rows, K/64 atoms, slots}  box {64, rows_per_cta, 2, 1}  -> [katom][rows][128B]
-//   MN-major (mode1): 4D {64, K rows, MN atoms, slots}  box {64, 128, natoms, 1}     -> [atom][128 K rows][128B]
-//   MN-major (mode2): 5D {64, 8, MN atoms, K/8, slots}  box {64, 8, natoms, 16, 1}   -> [kgroup][atom][8][128B]
+//   K-major:          4D {64, rows, K/64 atoms, slots}  box {64, rows_per_cta, PKA, 1}  -> [katom][rows][128B]
+//   MN-major (mode1): 4D {64, K rows, MN atoms, slots}  box {64, PBK, natoms, 1}       -> [atom][PBK K rows][128B]
+//   MN-major (mode2): 5D {64, 8, MN atoms, K/8, slots}  box {64, 8, natoms, PBK/8, 1}  -> [kgroup][atom][8][128B]
 __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_constant__ GemmParams P) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -124,7 +129,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
         TileCoord tc = tile_coord<2 * BM>(P, t);
         const Problem& pr = P.probs[tc.prob];
         const int bnc = pr.BN / 2;
-        const uint32_t bytes = (uint32_t)(BM + bnc) * 2u * ROW_BYTES * 2u;   // both CTAs, 2 K-atoms each
+        const uint32_t bytes = (uint32_t)(BM + bnc) * (uint32_t)PKA * ROW_BYTES * 2u;   // both CTAs, PKA K-atoms each
         const int am0 = tc.m0 + (int)crank * BM;
         // a spanning tile gives each CTA of the pair one whole N block; otherwise the two CTAs
         // split one block's BN columns
@@ -196,7 +201,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_pair_kernel(const __grid_
             const uint32_t da = sA + stage * PA_STAGE;
             const uint32_t db = sB + stage * PB_STAGE;
 #pragma unroll
-            for (int ka = 0; ka < 2; ++ka) {
+            for (int ka = 0; ka < PKA; ++ka) {
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk) {
                 const uint64_t ad = sdesc(da + ka * a_katom + kk * a_step, a_lbo, a_sbo);

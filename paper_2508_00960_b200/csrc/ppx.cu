@@ -304,20 +304,20 @@ struct Builder {
     if (!mn) {
       cuuint64_t dims[4] = {64, (cuuint64_t)v.rows, (cuuint64_t)(v.cols / 64), (cuuint64_t)v.slots};
       cuuint64_t strides[3] = {(cuuint64_t)v.ld * es, 128, (cuuint64_t)v.slot_stride * es};
-      cuuint32_t box[4] = {64, (cuuint32_t)rows_or_atoms, 2, 1};
+      cuuint32_t box[4] = {64, (cuuint32_t)rows_or_atoms, (cuuint32_t)ppx::PKA, 1};
       mode = 0;
       return add_map_nd(v, 4, dims, strides, box, -100);
     }
     if (interleaved) {
       cuuint64_t dims[5] = {64, 8, (cuuint64_t)(v.cols / 64), (cuuint64_t)(v.rows / 8), (cuuint64_t)v.slots};
       cuuint64_t strides[4] = {(cuuint64_t)v.ld * es, 128, (cuuint64_t)(8 * v.ld) * es, (cuuint64_t)v.slot_stride * es};
-      cuuint32_t box[5] = {64, 8, (cuuint32_t)rows_or_atoms, 16, 1};
+      cuuint32_t box[5] = {64, 8, (cuuint32_t)rows_or_atoms, (cuuint32_t)(ppx::PBK / 8), 1};
       mode = 2;
       return add_map_nd(v, 5, dims, strides, box, -101);
     }
     cuuint64_t dims[4] = {64, (cuuint64_t)v.rows, (cuuint64_t)(v.cols / 64), (cuuint64_t)v.slots};
     cuuint64_t strides[3] = {(cuuint64_t)v.ld * es, 128, (cuuint64_t)v.slot_stride * es};
-    cuuint32_t box[4] = {64, 128, (cuuint32_t)rows_or_atoms, 1};
+    cuuint32_t box[4] = {64, (cuuint32_t)ppx::PBK, (cuuint32_t)rows_or_atoms, 1};
     mode = 1;
     return add_map_nd(v, 4, dims, strides, box, -102);
   }
