@@ -204,6 +204,12 @@ class PhantomEngine:
         self.k3_fused = (k3_ok and self.group <= 2) if k3_fused is None else bool(k3_fused)
         if self.k3_fused:
             self.bwd_fused = False
+        # one GPU with every logical rank in one launch group: the error compression (p/2 slot-pair
+        # problems) rides in the first weight-gradient launch of the layer, error tiles first
+        # (<= 16 problems per launch; PPX_NO_K3G=1 keeps its own launch, A/B only)
+        self.k3_grouped = (not self.k3_fused and not self.bwd_fused and world == 1 and R > 1 and R % 2 == 0
+                           and self.group >= R and dtype == torch.bfloat16 and p % 2 == 0 and k % 64 == 0
+                           and not os.environ.get("PPX_NO_K3G"))
         # layer-0 compressor gradient with the batch split (ppx_wgrad_splitk): fp32 partial sums
         # (PPX_NO_SPLITK=1 keeps the one-launch form, A/B only)
         self.splitk_off = bool(os.environ.get("PPX_NO_SPLITK"))
@@ -536,7 +542,7 @@ class PhantomEngine:
             if self.capture_grads:
                 self.deltas[l] = [self.D[jj][cur].clone() for jj in range(R)]
             ios = [self._io(jj, l, par, x=self.D[jj][cur].data_ptr(), ld_x=s) for jj in range(R)]
-            if self.k3_fused:
+            if self.k3_fused or self.k3_grouped:
                 pass                      # error compression runs inside the weight-gradient launch
             elif nvrs:
                 # NVLink reduce-scatter: the error-compression epilogue copies every peer-owned
@@ -622,8 +628,23 @@ class PhantomEngine:
             per = max(1, min(self.group, 16 // nprob))
             nl = -(-R // per)
             per = -(-R // nl)
-            for c in range(0, R, per):
+            c = 0
+            if self.k3_grouped:
+                # error compression of all R ranks + the weight gradients of the first ranks
+                first = min(per, (16 - self.p // 2) // nprob)
+                nl2 = 1 + -(-(R - first) // per)
+                first = min(first, -(-R // nl2))          # balance the ranks over the launches
+                per = max(1, -(-(R - first) // max(1, nl2 - 1)))
+                flat = [it for chunk in per_rank[:first] for it in chunk]
+                arr = (_lib.WgradItem * len(flat))(*flat)
+                self._keep.append(arr)
+                self._call("ppx_backward_wgrad_errors", pdt, len(flat), arr, R, self._ios(ios), B,
+                           self.H[l].data_ptr(), None, 0, st,
+                           flops=sum(self._f_item(it) for it in flat) + R * self._f_error)
+                c = first
+            while c < R:
                 self._launch_wgrad([it for chunk in per_rank[c:c + per] for it in chunk], st)
+                c += per
             reduce_received()
             if l > 0:
                 ios = [self._recurrence_io(jj, l, par, cur) for jj in range(R)]
