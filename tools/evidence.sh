@@ -12,7 +12,7 @@ for g in 8 1; do
     python tools/engine_one.py 2 --group $g > gpurun_out/ev_ncu_list_g$g.log 2>&1
   echo "launch list g$g rc=$?"
 done
-for spec in "forward" "wgrad" "recurrence" "error" "forward --group 1" "wgrad_errors --group 1" "recurrence --group 1" "bwd --group 1 --k3 0"; do
+for spec in "forward" "wgrad" "wgrad_errors" "recurrence" "forward --group 1" "wgrad_errors --group 1" "recurrence --group 1" "bwd --group 1 --k3 0"; do
   tag=$(echo $spec | tr ' -' '__')
   timeout 200 python tools/kernel_probe.py $spec > gpurun_out/ev_probe_$tag.json 2>&1 && \
   timeout 400 ncu --set full --import-source on --clock-control none --profile-from-start off -f -o gpurun_out/ev_full_$tag \
@@ -22,6 +22,6 @@ for spec in "forward" "wgrad" "recurrence" "error" "forward --group 1" "wgrad_er
   # dominant kernel's (wgrad, N=1) report itself is kept
   ncu -i gpurun_out/ev_full_$tag.ncu-rep --page raw --csv > gpurun_out/ev_full_$tag.raw.csv 2>/dev/null
   ncu -i gpurun_out/ev_full_$tag.ncu-rep --page details > gpurun_out/ev_full_$tag.details.txt 2>/dev/null
-  [ "$tag" = "wgrad" ] || rm -f gpurun_out/ev_full_$tag.ncu-rep
+  [ "$tag" = "wgrad_errors" ] || rm -f gpurun_out/ev_full_$tag.ncu-rep
 done
 du -sh gpurun_out

@@ -2,9 +2,10 @@
 
     python tools/kernel_probe.py KIND [--group 1|8] [--iters 20] [--config c3] [--ncu]
 
-KIND: forward (fused / grouped forward), error (error compression), wgrad (grouped weight
-gradients), bwd (fused weight-gradient + recurrence launch, group=1 --k3 0), wgrad_errors (fused
-error-compression + weight-gradient launch, group=1), recurrence, compress — the middle launch of
+KIND: forward (fused / grouped forward), error (error compression as its own launch), wgrad
+(grouped weight gradients), bwd (fused weight-gradient + recurrence launch, group=1 --k3 0),
+wgrad_errors (fused error-compression + weight-gradient launch: the one-GPU default plan, or
+group=1), recurrence, compress — the middle launch of
 that kind in the step (--index to pick another).  The launches are issued exactly as
 PhantomEngine._step_body issues them (the engine records every kernel call of an eager step with
 its ABI arguments; the probe re-issues the chosen one) back to back behind a ~0.1 s device spin
@@ -34,6 +35,10 @@ ap.add_argument("--ncu", action="store_true")
 ap.add_argument("--k3", default="auto", help="k3_fused plan: auto|0|1")
 ap.add_argument("--noaccum", action="store_true", help="ppx_error_phantoms: overwrite instead of accumulate")
 args = ap.parse_args()
+if args.kind == "error" and not args.group:
+    # the default one-GPU plan runs the error compression inside the first weight-gradient launch
+    # of each layer (k3_grouped): probe the stand-alone launch of the alternative plan
+    os.environ.setdefault("PPX_NO_K3G", "1")
 cfg = bench.CONFIGS[args.config]
 eng = PhantomEngine(cfg["n"], cfg["p"], cfg["k"], cfg["layers"], cfg["batch"], lr=3e-6, group=args.group or None,
                     k3_fused=None if args.k3 == "auto" else args.k3 == "1")

@@ -21,8 +21,9 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
         "launch__grid_size", "launch__cluster_dim_x", "sm__cycles_active.avg"]
 CALL_OF = {"forward": "ppx_forward_fused", "wgrad": "ppx_wgrad", "recurrence": "ppx_backward_delta_n",
-           "error": "ppx_error_phantoms_n", "forward__group_1": "ppx_forward_n",
-           "wgrad_errors__group_1": "ppx_backward_wgrad_errors", "recurrence__group_1": "ppx_backward_delta_n (R=1)",
+           "error": "ppx_error_phantoms_n", "wgrad_errors": "ppx_backward_wgrad_errors",
+           "forward__group_1": "ppx_forward_n",
+           "wgrad_errors__group_1": "ppx_backward_wgrad_errors (R=1)", "recurrence__group_1": "ppx_backward_delta_n (R=1)",
            "bwd__group_1__k3_0": "ppx_backward_fused"}
 
 
