@@ -25,7 +25,7 @@ import os
 
 import torch
 
-from . import _lib, kernels
+from . import _lib, kernels, schedule
 from .core import Activation, as_activation, flat_offsets
 from .errors import ConfigurationError, TrainingError
 from .schedule import local_ranks
@@ -506,18 +506,8 @@ class PhantomEngine:
         return f
 
     def _layer0_split(self, n_items):
-        """Batch chunks of the layer-0 compressor gradient (ppx_wgrad_splitk, 128 x 256 tiles of
-        the 1-SM kernel for k <= 128): doubled while the doubled launch still fits one round on
-        the 148 SMs and the chunks stay whole 128-row K blocks, at most 16 problems per launch;
-        1 = unsplit."""
-        if self.splitk_off:
-            return 1
-        tiles = n_items * -(-self.k // 128) * -(-self.s // 256)
-        nsplit = 1
-        while (tiles * nsplit * 2 <= 148 and n_items * nsplit * 2 <= 16 and self.B % (nsplit * 2) == 0
-               and (self.B // (nsplit * 2)) % 128 == 0):
-            nsplit *= 2
-        return nsplit
+        """Batch chunks of the layer-0 compressor gradient (schedule.layer0_split); 1 = unsplit."""
+        return 1 if self.splitk_off else schedule.layer0_split(n_items, self.k, self.s, self.B)
 
     def _launch_wgrad(self, items, st):
         arr = (_lib.WgradItem * len(items))(*items)
@@ -625,26 +615,18 @@ class PhantomEngine:
                     cur = 1 - cur
                 continue
             nprob = 2 + (1 if l < L - 1 else 0) if self.p > 1 else 1
-            per = max(1, min(self.group, 16 // nprob))
-            nl = -(-R // per)
-            per = -(-R // nl)
-            c = 0
-            if self.k3_grouped:
-                # error compression of all R ranks + the weight gradients of the first ranks
-                first = min(per, (16 - self.p // 2) // nprob)
-                nl2 = 1 + -(-(R - first) // per)
-                first = min(first, -(-R // nl2))          # balance the ranks over the launches
-                per = max(1, -(-(R - first) // max(1, nl2 - 1)))
-                flat = [it for chunk in per_rank[:first] for it in chunk]
-                arr = (_lib.WgradItem * len(flat))(*flat)
-                self._keep.append(arr)
-                self._call("ppx_backward_wgrad_errors", pdt, len(flat), arr, R, self._ios(ios), B,
-                           self.H[l].data_ptr(), None, 0, st,
-                           flops=sum(self._f_item(it) for it in flat) + R * self._f_error)
-                c = first
-            while c < R:
-                self._launch_wgrad([it for chunk in per_rank[c:c + per] for it in chunk], st)
-                c += per
+            for i, (c0, c1) in enumerate(schedule.wgrad_launch_chunks(R, self.p, nprob, self.group,
+                                                                       self.k3_grouped)):
+                flat = [it for chunk in per_rank[c0:c1] for it in chunk]
+                if i == 0 and self.k3_grouped:
+                    # error compression of all R ranks + the weight gradients of the first ranks
+                    arr = (_lib.WgradItem * len(flat))(*flat)
+                    self._keep.append(arr)
+                    self._call("ppx_backward_wgrad_errors", pdt, len(flat), arr, R, self._ios(ios), B,
+                               self.H[l].data_ptr(), None, 0, st,
+                               flops=sum(self._f_item(it) for it in flat) + R * self._f_error)
+                else:
+                    self._launch_wgrad(flat, st)
             reduce_received()
             if l > 0:
                 ios = [self._recurrence_io(jj, l, par, cur) for jj in range(R)]

@@ -60,3 +60,42 @@ def tp_comm_bytes_per_step(n: int, layers: int, batch: int, world: int, elem: in
         return 0
     pairs = layers // 2
     return int(2 * pairs * 2 * (world - 1) / world * batch * n * elem)
+
+
+MAX_PROBS = 16   # problems per grouped GEMM launch (csrc/gemm_sm100.cuh)
+
+
+def wgrad_launch_chunks(R: int, p: int, nprob: int, group: int, with_errors: bool) -> list[tuple[int, int]]:
+    """Logical-rank ranges [c0, c1) of one layer's weight-gradient launches (`nprob` problems per
+    rank, <= MAX_PROBS per launch, at most `group` ranks per launch, balanced).  with_errors: the
+    first launch also carries the layer's error compression as p/2 slot-pair problems (the
+    one-GPU default plan, engine.k3_grouped)."""
+    per = max(1, min(group, MAX_PROBS // nprob))
+    nl = -(-R // per)
+    per = -(-R // nl)
+    out, c = [], 0
+    if with_errors:
+        first = min(per, (MAX_PROBS - p // 2) // nprob)
+        if first < 1:
+            raise ConfigurationError(f"{p // 2} error problems leave no room for weight gradients")
+        nl2 = 1 + -(-(R - first) // per)
+        first = min(first, -(-R // nl2))          # balance the ranks over the launches
+        per = max(1, -(-(R - first) // max(1, nl2 - 1)))
+        out.append((0, first))
+        c = first
+    while c < R:
+        out.append((c, min(R, c + per)))
+        c += per
+    return out
+
+
+def layer0_split(n_items: int, k: int, s: int, batch: int) -> int:
+    """Batch chunks of the layer-0 compressor gradient (ppx_wgrad_splitk, 128 x 256 tiles of the
+    1-SM kernel): doubled while the doubled launch still fits one round on the 148 SMs, every
+    chunk stays whole 128-row K blocks and the launch holds <= MAX_PROBS problems; 1 = unsplit."""
+    tiles = n_items * -(-k // 128) * -(-s // 256)
+    nsplit = 1
+    while (tiles * nsplit * 2 <= 148 and n_items * nsplit * 2 <= MAX_PROBS and batch % (nsplit * 2) == 0
+           and (batch // (nsplit * 2)) % 128 == 0):
+        nsplit *= 2
+    return nsplit
