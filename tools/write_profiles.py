@@ -22,9 +22,10 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__grid_size", "launch__cluster_dim_x", "sm__cycles_active.avg"]
 CALL_OF = {"forward": "ppx_forward_fused", "wgrad": "ppx_wgrad", "recurrence": "ppx_backward_delta_n",
            "error": "ppx_error_phantoms_n", "wgrad_errors": "ppx_backward_wgrad_errors",
-           "forward__group_1": "ppx_forward_n",
-           "wgrad_errors__group_1": "ppx_backward_wgrad_errors (R=1)", "recurrence__group_1": "ppx_backward_delta_n (R=1)",
-           "bwd__group_1__k3_0": "ppx_backward_fused"}
+           "forward___group_1": "ppx_forward_n",
+           "wgrad_errors___group_1": "ppx_backward_wgrad_errors (R=1)",
+           "recurrence___group_1": "ppx_backward_delta_n (R=1)",
+           "bwd___group_1___k3_0": "ppx_backward_fused"}   # tags: the probe spec with ' -' -> '_' (evidence.sh)
 
 
 def raw_metrics(path):
