@@ -195,7 +195,9 @@ class PhantomEngine:
         if bwd_fused and (dtype != torch.bfloat16 or self.group > 3):
             raise ConfigurationError("fused backward needs bf16 and <= 3 logical ranks per launch group")
         self.bwd_fused = auto_bf if bwd_fused is None else bool(bwd_fused)
-        # error compression + weight gradients in one launch (<= 16 problems: p slots + 3 per rank)
+        # error compression + weight gradients in one launch (<= 16 problems: p slots + 3 per rank;
+        # 4 ranks per GPU with slot pairs would fit 16 too, but its small-shape 2-GPU parity run
+        # flagged non-finite gradients: not enabled, profiles/r2_ab_k3_n2.txt)
         k3_ok = (dtype == torch.bfloat16 and p > 1 and p + 3 * self.group <= 16 and
                  ((world > 1 and self.nvrs and self.group == R) or (world == 1 and self.group < R)))
         if k3_fused and not k3_ok:

@@ -12,6 +12,7 @@ ap.add_argument("--config", default="c3")
 ap.add_argument("--steps", type=int, default=40)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--group", type=int, default=0, help="logical ranks per launch (1 = the 8-GPU per-GPU shapes)")
+ap.add_argument("--k3", default="auto", choices=["auto", "0", "1"], help="k3_fused plan A/B")
 a = ap.parse_args()
 cfg = bench.CONFIGS[a.config]
 world, rank, local = int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0))
@@ -20,7 +21,8 @@ if world > 1:
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 D = bench.Dist(world, rank, local)
 eng = PhantomEngine(cfg["n"], cfg["p"], cfg["k"], cfg["layers"], cfg["batch"], world=world, rank=rank, device=local,
-                    uid=D.uid(), lr=3e-6, group=a.group or None)
+                    uid=D.uid(), lr=3e-6, group=a.group or None,
+                    k3_fused=None if a.k3 == "auto" else a.k3 == "1")
 xs, ts = bench.make_data(eng, 1234, cfg)
 eng.set_batch(xs, ts, 0)
 eng.set_batch(xs, ts, 1)
@@ -31,7 +33,7 @@ for _ in range(5):
 ms = [bench.timed_steps(eng, D, a.steps) for _ in range(a.reps)]
 if rank == 0:
     env = {k: v for k, v in os.environ.items() if k.startswith(("PPX_DEBUG", "PPX_NO_", "PPX_AB_"))}
-    print(json.dumps({"config": a.config, "world": world, "group": eng.group, "env": env, "ms": ms}))
+    print(json.dumps({"config": a.config, "world": world, "group": eng.group, "k3": eng.k3_fused, "env": env, "ms": ms}))
 D.barrier()
 eng.close()
 bench.finish(D)
