@@ -60,6 +60,15 @@ def test_two_gpus_tensor_parallel(dtype):
     _run(2, "mp_tp_parity.py", "--dtype", dtype)
 
 
+def test_two_gpus_default_path_four_ranks():
+    """The default plan of C3 on 2 GPUs — four logical ranks per GPU (p = 8): fused compression +
+    NVLink all-gather + forward, error compression with slot-pair tiles scattered to the owners
+    over NVLink (4 contributing ranks per pair), grouped weight gradients, in-kernel reduce; vs
+    the oracle."""
+    out = _run(2, "mp_parity.py", "--dtype", "bf16", "--p", 8, "--width", 1024, "--k", 64, "--B", 256, "--lr", "1e-4")
+    assert '"fused": true' in out
+
+
 @pytest.mark.parametrize("p,n", [(4, 512), (8, 1024)])
 def test_four_gpus_default_path(p, n):
     """The default multi-GPU plan on 4 GPUs (bf16, k = 64): fused compression + NVLink all-gather +
