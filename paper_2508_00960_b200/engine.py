@@ -195,15 +195,18 @@ class PhantomEngine:
         if bwd_fused and (dtype != torch.bfloat16 or self.group > 3):
             raise ConfigurationError("fused backward needs bf16 and <= 3 logical ranks per launch group")
         self.bwd_fused = auto_bf if bwd_fused is None else bool(bwd_fused)
-        # error compression + weight gradients in one launch (<= 16 problems: p slots + 3 per rank;
-        # 4 ranks per GPU with slot pairs would fit 16 too, but its small-shape 2-GPU parity run
-        # flagged non-finite gradients: not enabled, profiles/r2_ab_k3_n2.txt)
-        k3_ok = (dtype == torch.bfloat16 and p > 1 and p + 3 * self.group <= 16 and
+        # error compression + weight gradients in one launch (<= 16 problems: p slots, or p/2 slot
+        # pairs, + 3 per rank)
+        pairs = p % 2 == 0 and k % 64 == 0 and (self.group % 2 == 0 or self.group == 1)
+        n_err = p // 2 if pairs else p
+        k3_ok = (dtype == torch.bfloat16 and p > 1 and n_err + 3 * self.group <= 16 and
                  ((world > 1 and self.nvrs and self.group == R) or (world == 1 and self.group < R)))
         if k3_fused and not k3_ok:
             raise ConfigurationError("fused error compression + weight gradients needs bf16, p + 3 ranks per launch "
                                      "<= 16 and either the NVLink reduce-scatter or one GPU with per-group launches")
-        self.k3_fused = (k3_ok and self.group <= 2) if k3_fused is None else bool(k3_fused)
+        # default with <= 2 ranks per launch, and on every multi-GPU run the limit admits (C3 at
+        # N = 2: 4 slot pairs + 4 ranks x 3 = 16 problems)
+        self.k3_fused = (k3_ok and (self.group <= 2 or world > 1)) if k3_fused is None else bool(k3_fused)
         if self.k3_fused:
             self.bwd_fused = False
         # one GPU with every logical rank in one launch group: the error compression (p/2 slot-pair

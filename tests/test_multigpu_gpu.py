@@ -60,12 +60,15 @@ def test_two_gpus_tensor_parallel(dtype):
     _run(2, "mp_tp_parity.py", "--dtype", dtype)
 
 
-def test_two_gpus_default_path_four_ranks():
-    """The default plan of C3 on 2 GPUs — four logical ranks per GPU (p = 8): fused compression +
-    NVLink all-gather + forward, error compression with slot-pair tiles scattered to the owners
-    over NVLink (4 contributing ranks per pair), grouped weight gradients, in-kernel reduce; vs
-    the oracle."""
-    out = _run(2, "mp_parity.py", "--dtype", "bf16", "--p", 8, "--width", 1024, "--k", 64, "--B", 256, "--lr", "1e-4")
+@pytest.mark.parametrize("k3", ["auto", "0"])
+def test_two_gpus_default_path_four_ranks(k3):
+    """C3's plan on 2 GPUs — four logical ranks per GPU (p = 8): fused compression + NVLink
+    all-gather + forward; error compression as slot-pair tiles (4 contributing ranks per pair)
+    scattered to the owners over NVLink — inside the weight-gradient launch (k3 default: 4 pair
+    problems + 12 weight-gradient problems) or as its own launch (k3 = 0) — in-kernel reduce; vs
+    the oracle.  (lr 1e-4: at 3e-3 this bf16 model diverges within 3 steps on every plan.)"""
+    out = _run(2, "mp_parity.py", "--dtype", "bf16", "--p", 8, "--width", 1024, "--k", 64, "--B", 256, "--lr", "1e-4",
+               "--k3", k3)
     assert '"fused": true' in out
 
 
