@@ -50,3 +50,21 @@ def test_layer0_split(n_items, k, s, batch, expect):
     assert tiles * nsplit <= 148 or nsplit == 1
     assert batch % nsplit == 0 and (nsplit == 1 or (batch // nsplit) % 128 == 0)
     assert n_items * nsplit <= schedule.MAX_PROBS
+
+
+@pytest.mark.parametrize("knob", ["PPX_NO_SPLITK", "PPX_NO_K3G", "PPX_AB_TF32_HI_COPY", "PPX_DEBUG_EPI", "PPX_QBAL"])
+def test_bench_refuses_plan_knobs(knob, monkeypatch):
+    """The bench line is always the default plan: every A/B or debug switch is refused."""
+    import bench
+    monkeypatch.setenv(knob, "1")
+    with pytest.raises(SystemExit):
+        bench.refuse_debug_knobs()
+
+
+def test_bench_allows_library_path(monkeypatch):
+    import bench
+    for k in [k for k in list(__import__("os").environ) if k.startswith("PPX_")]:
+        monkeypatch.delenv(k, raising=False)
+    monkeypatch.setenv("PPX_NO_NUMA_BIND", "1")
+    monkeypatch.setenv("PPX_LIB", "/tmp/libppx.so")
+    bench.refuse_debug_knobs()
