@@ -118,9 +118,10 @@ ppx_status ppx_reserve_workspace(ppx_ctx* ctx, int64_t bytes);
 /* FP32 tier (3xTF32): between on = 1 and on = 0, the low part (x - tf32(x)) of every GEMM operand
    read on `stream` is split once and reused by later calls until a ppx call writes an
    overlapping range.  The caller guarantees that nothing but ppx calls writes those operands
-   inside the scope (the engine brackets one training / inference step) and orders consecutive
-   scopes (same stream, or a device synchronisation in between).  No kernel launch; host-side
-   bookkeeping only.  Engine-internal: the reference splits nothing (numpy float64). */
+   inside the scope (the engine brackets one training / inference step).  A scope on another
+   stream than the previous one waits for it (event) before reusing the pooled buffers, except
+   under stream capture (the engine synchronises the device before capturing).  No kernel
+   launch.  Engine-internal: the reference splits nothing (numpy float64). */
 ppx_status ppx_tf32_scope(ppx_ctx* ctx, int32_t on, void* stream);
 
 /* ---- phantom-parallel layer ops -------------------------------------------------------- */

@@ -48,6 +48,8 @@ struct ppx_ctx {
   long long launches = 0;   // kernels this context enqueued (ppx_kernel_launches)
   bool lo_scope = false;
   cudaStream_t lo_stream = nullptr;
+  cudaEvent_t lo_done = nullptr;   // recorded when a scope ends: the next scope's stream waits on it
+  bool lo_done_valid = false;
   std::map<std::pair<const char*, int64_t>, LoEntry> lo_live;   // (operand base, elements) -> low part
   std::multimap<size_t, char*> lo_pool;                         // free buffers by capacity
   std::vector<char*> lo_all;
@@ -933,6 +935,7 @@ ppx_status ppx_destroy(ppx_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (auto& c : ctx->ws) cudaFree(c.first);
   for (char* m : ctx->lo_all) cudaFree(m);
+  if (ctx->lo_done) cudaEventDestroy(ctx->lo_done);
   for (void* m : ctx->ipc_mapped) cudaIpcCloseMemHandle(m);
   if (ctx->fuse_done) cudaFree(ctx->fuse_done);
   if (ctx->reduce_done) cudaFree(ctx->reduce_done);
@@ -1878,9 +1881,22 @@ ppx_status ppx_gemm_update(ppx_ctx* ctx, ppx_dtype dt, int32_t M, int32_t N, int
 
 ppx_status ppx_tf32_scope(ppx_ctx* ctx, int32_t on, void* stream) {
   if (!ctx) return PPX_E_CONFIG;
+  const cudaStream_t st = (cudaStream_t)stream;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  const bool capturing = cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+  if (on && !ctx->lo_pool.empty() && ctx->lo_done_valid && st != ctx->lo_stream && !capturing) {
+    // the pooled buffers were last used on another stream: order this scope after that one
+    // (a capture is preceded by a device synchronisation in the engine)
+    CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->lo_done, 0));
+  }
   lo_clear(ctx);
+  if (!on && ctx->lo_scope && !capturing && ctx->lo_stream == st) {
+    if (!ctx->lo_done) CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->lo_done, cudaEventDisableTiming));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->lo_done, st));
+    ctx->lo_done_valid = true;
+  }
   ctx->lo_scope = on != 0;
-  ctx->lo_stream = (cudaStream_t)stream;
+  ctx->lo_stream = st;
   return PPX_OK;
 }
 

@@ -104,3 +104,31 @@ def test_engine_launch_count_is_the_library_count():
         counts[dt] = eng.launch_count
         eng.close()
     assert counts[torch.float32] > counts[torch.bfloat16]
+
+
+def test_scopes_on_different_streams_are_ordered():
+    """Consecutive scopes on different streams, no host synchronisation: the second scope's
+    splits reuse the pooled buffers only after the first scope's work (event wait)."""
+    from paper_2508_00960_b200 import _lib, kernels
+    ctx = _lib.default_context(0)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn(2048, 2048, device="cuda", generator=g)
+    b = torch.randn(2048, 2048, device="cuda", generator=g)
+    a2 = torch.randn(2048, 2048, device="cuda", generator=g)
+    c1 = torch.empty(2048, 2048, device="cuda")
+    c2 = torch.empty(2048, 2048, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    s1.wait_stream(torch.cuda.current_stream())
+    s2.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s1):
+        ctx.call("ppx_tf32_scope", 1, s1.cuda_stream)
+        for _ in range(3):
+            kernels.gemm(a, b, out=c1)
+        ctx.call("ppx_tf32_scope", 0, s1.cuda_stream)
+    with torch.cuda.stream(s2):
+        ctx.call("ppx_tf32_scope", 1, s2.cuda_stream)
+        kernels.gemm(a2, b, out=c2)
+        ctx.call("ppx_tf32_scope", 0, s2.cuda_stream)
+    torch.cuda.synchronize()
+    assert _err(c1, _ref(a, b)) < 1e-5
+    assert _err(c2, _ref(a2, b)) < 1e-5
